@@ -1,0 +1,211 @@
+"""Drop-in cluster: epdsim's own event loop with the GPU executor underneath.
+
+``GpuCluster`` subclasses the reference ``Cluster`` (cluster.py:168-488) and keeps its
+event loop, router, stage-level batching, admission and migration protocol.  Three
+seams change:
+
+  S1  ``_try_schedule`` (cluster.py:287-299): the batch formed by the reference
+      ``form_batch`` runs on the instance's GPU via ``InstanceRuntime.run_batch``; its
+      latency is epdsim's own ``batch_latency`` (clock="oracle") or measured
+      (clock="device" | "wall").
+  S2  each instance's ``kv_pool`` / ``image_pool`` is replaced, before any request
+      arrives, by a ``PhysicalCachePool`` with the same capacity.
+  S3  ``_start_migration`` (cluster.py:392-421) wraps the job in ``GpuMigrationJob``
+      whose ``transfer_seconds`` (migration.py:63-64) performs the block copy -- KV
+      blocks for PD, image-cache blocks for EP -- when the target reserves its blocks
+      (first call, cluster.py:323) and returns the cached value on the accounting call
+      (cluster.py:437).
+
+Instances map to devices in construction order (E, P, D, EP, ED, PD, EPD;
+cluster.py:180-190): instance k -> devices[k % len(devices)].  Copies between
+instances on different GPUs read the source pool through a peer (NVLink) pointer.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import hashlib
+import json
+from typing import Dict, List, Optional, Sequence
+
+import torch
+
+from . import _lib
+from ._epdsim import C, EN, MC, MG
+from .executor import CLOCKS, InstanceRuntime
+from .inputs import ImageStore
+from .shapes import MllmShape
+from .weights import DeviceWeights
+
+
+class GpuMigrationJob(MG.MigrationJob):
+    """MigrationJob whose transfer is a real block copy; the measured (or oracle)
+    duration is computed once and cached, because the loop asks twice."""
+
+    def bind(self, cluster: "GpuCluster") -> "GpuMigrationJob":
+        self._cluster = cluster
+        self._seconds = None
+        return self
+
+    def transfer_seconds(self, hw) -> float:
+        if self._seconds is None:
+            self._seconds = self._cluster._execute_transfer(self, hw)
+        return self._seconds
+
+
+class GpuCluster(C.Cluster):
+    def __init__(self, spec, shape: MllmShape, hw, slo, *, devices: Sequence = None,
+                 clock: str = "device", seed: int = 0, resident_inputs: bool = True,
+                 probe_image_tokens: int = MC.IMAGE_BLOCK_TOKENS, max_slots: int = 4096,
+                 max_seq_tokens: int = 16384, record_batches: bool = False,
+                 weights: Optional[Dict] = None, capture: bool = False,
+                 pool_bytes_limit: Optional[int] = None):
+        if clock not in CLOCKS:
+            raise ValueError(f"clock must be one of {CLOCKS}")
+        if not torch.cuda.is_available():
+            raise RuntimeError("GpuCluster needs a CUDA device (there is no CPU fallback)")
+        super().__init__(spec, shape.profile(), hw, slo, probe_image_tokens)
+        self.shape = shape
+        self.clock = clock
+        self.seed = seed
+        devices = [torch.device(d) for d in (devices or [torch.device("cuda", 0)])]
+        self.devices = devices
+        self.images = ImageStore(seed, shape.patch)
+        self.weights: Dict[torch.device, DeviceWeights] = dict(weights or {})
+        self.runtimes: Dict[str, InstanceRuntime] = {}
+        for k, (iid, inst) in enumerate(self.instances.items()):
+            dev = devices[k % len(devices)]
+            if dev not in self.weights:
+                self.weights[dev] = DeviceWeights(shape, dev, seed)
+            self.runtimes[iid] = InstanceRuntime(
+                inst, shape, self.weights[dev], seed=seed, images=self.images,
+                resident_inputs=resident_inputs, max_slots=max_slots,
+                max_seq_tokens=max_seq_tokens, capture=capture,
+                pool_bytes_limit=pool_bytes_limit)
+        if len({d.index for d in devices}) > 1:
+            for a in devices:
+                for b in devices:
+                    if a != b:
+                        _lib.check(_lib.load().hy_enable_peer_access(a.index, b.index),
+                                   "hy_enable_peer_access")
+        self.capture = capture
+        self.exec_order: List = []
+        self.batch_log: Optional[List] = [] if record_batches else None
+        self.migration_log: List = []
+        self.transfer_stats = {"count": 0, "bytes": 0.0, "copied_bytes": 0, "seconds": 0.0}
+        self.generated: Dict[str, List[int]] = {}
+
+    # ------------------------------------------------------------------ S1
+    def _try_schedule(self, iid: str) -> None:
+        inst = self.instances[iid]
+        if inst.busy:
+            return
+        self._admit_migrations(inst)
+        batch = inst.form_batch(self.reqs)
+        if not batch:
+            return
+        latency = self.runtimes[iid].run_batch(batch, self.reqs, self.clock, self.model,
+                                               self.hw)
+        if self.capture:
+            self.exec_order.append((iid, len(self.runtimes[iid].exec_log) - 1))
+        if self.batch_log is not None:
+            self.batch_log.append((iid, tuple(batch.decode_entries),
+                                   tuple(batch.prefill_chunks),
+                                   tuple(batch.encode_entries), repr(latency)))
+        inst.busy = True
+        inst.current_batch = batch
+        inst.current_latency = latency
+        self._push(self.now + latency, C._BATCH_DONE, iid)
+
+    # ------------------------------------------------------------------ S3
+    def _start_migration(self, r, inst, kind: str) -> None:
+        super()._start_migration(r, inst, kind)
+        job = self.jobs[r.rid]
+        fields = {f.name: getattr(job, f.name) for f in dataclasses.fields(job)}
+        self.jobs[r.rid] = GpuMigrationJob(**fields).bind(self)
+
+    def _execute_transfer(self, job: GpuMigrationJob, hw) -> float:
+        src = self.runtimes[job.source]
+        dst = self.runtimes[job.target]
+        r = self.reqs[job.rid]
+        lib = _lib.load()
+        kv_n = MC.kv_blocks_needed(r.kv_len) if job.kv_bytes > 0 else 0
+        img_n = job.image_blocks if job.image_bytes > 0 else 0
+        maps = []
+        if kv_n:
+            s_ids = src.kv_pool.ids[job.rid][:kv_n]
+            d_ids = dst.kv_pool.ids[job.rid][:kv_n]
+            maps.append(("kv", s_ids, d_ids, src.kv, dst.kv, self.shape.kv_block_elems * 2))
+        if img_n:
+            s_ids = src.image_pool.ids[job.rid][:img_n]
+            d_ids = dst.image_pool.ids[job.rid][:img_n]
+            maps.append(("image", s_ids, d_ids, src.img, dst.img,
+                         self.shape.image_block_elems * 2))
+        dev = dst.device  # pull-based: the target's SMs read the source pool
+        torch.cuda.set_device(dev)
+        stream = torch.cuda.current_stream(dev)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ids_dev = []
+        for _, s_ids, d_ids, *_ in maps:
+            ids_dev.append(torch.tensor(list(s_ids) + list(d_ids), dtype=torch.int32).to(dev))
+        # the source's last batch must be complete before its blocks are read
+        torch.cuda.synchronize(src.device)
+        ev0.record(stream)
+        copied = 0
+        for (what, s_ids, d_ids, s_pool, d_pool, block_bytes), ids in zip(maps, ids_dev):
+            n = len(s_ids)
+            _lib.check(lib.hy_copy_blocks(s_pool.data_ptr(), d_pool.data_ptr(), ids.data_ptr(),
+                                          ids.data_ptr() + 4 * n, n, block_bytes,
+                                          stream.cuda_stream), "hy_copy_blocks")
+            copied += n * block_bytes
+        if job.kind == "pd":
+            ss = src.kv_pool.slot[job.rid]
+            ds = dst.kv_pool.slot[job.rid]
+            dst.last_tok[ds:ds + 1].copy_(src.last_tok[ss:ss + 1], non_blocking=True)
+        ev1.record(stream)
+        ev1.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        self.transfer_stats["count"] += 1
+        self.transfer_stats["bytes"] += job.kv_bytes + job.image_bytes
+        self.transfer_stats["copied_bytes"] += copied
+        self.transfer_stats["seconds"] += ms * 1e-3
+        self.migration_log.append((job.kind, job.source, job.target, job.rid,
+                                   [(w, list(s), list(d)) for w, s, d, *_ in maps], ms))
+        if self.clock == "oracle":
+            return MG.MigrationJob.transfer_seconds(job, hw)
+        return ms * 1e-3
+
+    # ------------------------------------------------------------------ results
+    def _finish(self, r, inst) -> None:
+        super()._finish(r, inst)
+        self.runtimes[inst.id].forget(r.rid)
+
+    def run(self, trace, check_invariants: bool = False):
+        report = super().run(trace, check_invariants=check_invariants)
+        for rt in self.runtimes.values():
+            rt.collect_tokens(self.generated)
+        return report
+
+    def _assert_invariants(self) -> None:
+        super()._assert_invariants()
+        for iid, rt in self.runtimes.items():
+            for pool in (rt.kv_pool, rt.image_pool):
+                if not pool.consistent():
+                    raise AssertionError(f"physical pool of {iid} disagrees with its counts")
+
+    def gpu_launch_count(self) -> int:
+        return sum(rt.launches for rt in self.runtimes.values())
+
+
+def batch_log_digest(log) -> str:
+    """sha256[:16] of a batch log, the recipe in BASELINE.md section 2."""
+    return hashlib.sha256(json.dumps(log).encode()).hexdigest()[:16]
+
+
+def run_trace_gpu(spec, shape: MllmShape, hw, slo, trace, *, check_invariants: bool = False,
+                  **kw):
+    """GPU counterpart of ``epdsim.run_trace`` (cluster.py:491-497)."""
+    cluster = GpuCluster(spec, shape, hw, slo, **kw)
+    report = cluster.run(trace, check_invariants=check_invariants)
+    return cluster, report

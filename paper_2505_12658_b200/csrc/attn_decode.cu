@@ -1,0 +1,238 @@
+// K8: paged-KV decode attention (one query token per running decode entry).
+//
+// The dominant HBM stream at large decode batches: every step reads the whole cached
+// context of every running request, bytes = sum_i (S_i + 1) * kv_bytes_per_token
+// (epdsim charges 2*B*H*(S+1)*ratio per layer, model_cost.py:195).
+//
+// Layout read: KV pool block [layer][K|V][kv_head][16 tok][d], so one (block, head) K
+// tile is 16 x d contiguous bf16 (4 KiB at d = 128).
+//
+// Grid (seq, kv_head, split).  Each of the 4 warps streams whole 16-token blocks:
+// a warp-wide 16-byte load covers 2 tokens x 128 dims, 8 loads cover the block's K and
+// 8 more its V, all issued before use.  Scores reduce across 16 lanes with xor
+// shuffles, softmax is online (exp2 domain), all G = n_heads / n_kv_heads query heads
+// of a KV head share each K/V load (GQA).  Warps merge through shared memory; when the
+// context is split across CTAs (flash-decoding) a second kernel merges the partials.
+#include "common.cuh"
+#include "../../include/hydra_sm100.h"
+
+#include <algorithm>
+
+namespace hy {
+
+constexpr int DEC_WARPS = 4;
+
+template <int G>
+__global__ void __launch_bounds__(128)
+    attn_decode_kernel(const bf16* __restrict__ q, int ld_q, int n_kv, const int* __restrict__ slots,
+                       const int* __restrict__ ctx_len, const int* __restrict__ block_table,
+                       int bt_stride, const bf16* __restrict__ kv, long long block_stride,
+                       float scale_log2, int blocks_per_split, bf16* __restrict__ out, int ld_o,
+                       float* __restrict__ part, int nsplit) {
+  constexpr int D = 128;
+  const int b = blockIdx.x, kh = blockIdx.y, sp = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, dl = lane & 15;
+  const int n_heads = n_kv * G;
+  const int ctx = ctx_len[b];
+  const int nblk = (ctx + HY_KV_BLOCK_TOKENS - 1) / HY_KV_BLOCK_TOKENS;
+  const int blk0 = sp * blocks_per_split;
+  const int blk1 = min(nblk, blk0 + blocks_per_split);
+  const int* bt = block_table + (size_t)slots[b] * bt_stride;
+
+  float qf[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    load_bf16x8(q + (size_t)b * ld_q + (size_t)(kh * G + g) * D + dl * 8, qf[g]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) qf[g][j] *= scale_log2;
+  }
+  float m[G], l[G], acc[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[g][j] = 0.f;
+  }
+
+  const size_t head_off = (size_t)kh * HY_KV_BLOCK_TOKENS * D;
+  const size_t v_off = (size_t)n_kv * HY_KV_BLOCK_TOKENS * D;
+  for (int jb = blk0 + warp; jb < blk1; jb += DEC_WARPS) {
+    const bf16* kb = kv + (size_t)bt[jb] * block_stride + head_off;
+    const bf16* vb = kb + v_off;
+    uint4 kr[8], vr[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) kr[i] = ld_nc_v4(kb + (size_t)(2 * i + half) * D + dl * 8);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) vr[i] = ld_nc_v4(vb + (size_t)(2 * i + half) * D + dl * 8);
+    const int tok_base = jb * HY_KV_BLOCK_TOKENS + half;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float s[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float2 k0 = unpack_bf16x2(kr[i].x), k1 = unpack_bf16x2(kr[i].y),
+               k2 = unpack_bf16x2(kr[i].z), k3 = unpack_bf16x2(kr[i].w);
+        float d0 = qf[g][0] * k0.x + qf[g][1] * k0.y + qf[g][2] * k1.x + qf[g][3] * k1.y +
+                   qf[g][4] * k2.x + qf[g][5] * k2.y + qf[g][6] * k3.x + qf[g][7] * k3.y;
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 8);
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 4);
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
+        s[i] = (tok_base + 2 * i < ctx) ? d0 : -INFINITY;
+      }
+      float mb = s[0];
+#pragma unroll
+      for (int i = 1; i < 8; ++i) mb = fmaxf(mb, s[i]);
+      mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
+      const float mn = fmaxf(m[g], mb);  // finite: every block holds >= 1 valid token
+      const float corr = exp2f(m[g] - mn);
+      m[g] = mn;
+      float ls = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[g][j] *= corr;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float p = exp2f(s[i] - mn);
+        ls += p;
+        float2 v0 = unpack_bf16x2(vr[i].x), v1 = unpack_bf16x2(vr[i].y),
+               v2 = unpack_bf16x2(vr[i].z), v3 = unpack_bf16x2(vr[i].w);
+        acc[g][0] += p * v0.x; acc[g][1] += p * v0.y;
+        acc[g][2] += p * v1.x; acc[g][3] += p * v1.y;
+        acc[g][4] += p * v2.x; acc[g][5] += p * v2.y;
+        acc[g][6] += p * v3.x; acc[g][7] += p * v3.y;
+      }
+      l[g] = l[g] * corr + ls;
+    }
+  }
+  // merge the two half-warps (same m, disjoint tokens)
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    l[g] += __shfl_xor_sync(0xffffffffu, l[g], 16);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[g][j] += __shfl_xor_sync(0xffffffffu, acc[g][j], 16);
+  }
+  // merge warps through shared memory
+  __shared__ float sm_m[DEC_WARPS][G], sm_l[DEC_WARPS][G];
+  __shared__ float sm_acc[DEC_WARPS][G][D];
+  if (half == 0) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sm_acc[warp][g][dl * 8 + j] = acc[g][j];
+      if (dl == 0) {
+        sm_m[warp][g] = m[g];
+        sm_l[warp][g] = l[g];
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < G * D; e += blockDim.x) {
+    const int g = e / D, d = e % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < DEC_WARPS; ++w) M = fmaxf(M, sm_m[w][g]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < DEC_WARPS; ++w) {
+        const float f = exp2f(sm_m[w][g] - M);
+        L += sm_l[w][g] * f;
+        O += sm_acc[w][g][d] * f;
+      }
+    }
+    const int hq = kh * G + g;
+    if (nsplit == 1) {
+      out[(size_t)b * ld_o + (size_t)hq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+    } else {
+      float* pp = part + (((size_t)b * n_heads + hq) * nsplit + sp) * (D + 2);
+      pp[d] = O;
+      if (d == 0) {
+        pp[D] = M;
+        pp[D + 1] = L;
+      }
+    }
+  }
+}
+
+__global__ void attn_decode_combine_kernel(const float* __restrict__ part, int n_heads, int nsplit,
+                                           bf16* __restrict__ out, int ld_o) {
+  constexpr int D = 128;
+  const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
+  const float* pp = part + ((size_t)b * n_heads + h) * nsplit * (D + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, pp[s * (D + 2) + D]);
+  float L = 0.f, O = 0.f;
+  if (M != -INFINITY) {
+    for (int s = 0; s < nsplit; ++s) {
+      const float f = exp2f(pp[s * (D + 2) + D] - M);
+      L += pp[s * (D + 2) + D + 1] * f;
+      O += pp[s * (D + 2) + d] * f;
+    }
+  }
+  out[(size_t)b * ld_o + (size_t)h * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+}
+
+static int decode_splits(int n, int n_kv, int max_ctx) {
+  const int max_blocks = std::max(1, ceil_div(max_ctx, HY_KV_BLOCK_TOKENS));
+  const int target = num_sms() * 8;
+  int ns = ceil_div(target, std::max(1, n * n_kv));
+  ns = std::min(ns, std::max(1, max_blocks / 4));  // >= 4 blocks per split: one per warp
+  return std::max(1, std::min(ns, 64));
+}
+
+}  // namespace hy
+
+using namespace hy;
+
+extern "C" size_t hy_attn_decode_workspace_bytes(int n, int n_heads, int head_dim, int max_ctx) {
+  const int ns = decode_splits(n, n_heads, max_ctx);  // n_kv <= n_heads: upper bound
+  return (size_t)n * n_heads * std::max(ns, 64) * (head_dim + 2) * sizeof(float);
+}
+
+extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads, int n_kv_heads,
+                                    int head_dim, const int* slots, const int* ctx, int max_ctx,
+                                    const int* block_table, int bt_stride, const void* kv_layer,
+                                    long long block_stride, float scale, void* out, int ld_o,
+                                    void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+  HY_CHECK_ARG(head_dim == 128, "decode attention supports head_dim 128");
+  HY_CHECK_ARG(n_kv_heads > 0 && n_heads % n_kv_heads == 0, "heads");
+  if (n <= 0) return 0;
+  const int G = n_heads / n_kv_heads;
+  int ns = decode_splits(n, n_kv_heads, max_ctx);
+  const size_t need = (size_t)n * n_heads * ns * (head_dim + 2) * sizeof(float);
+  if (ns > 1 && (workspace == nullptr || need > workspace_bytes)) ns = 1;
+  const int max_blocks = std::max(1, ceil_div(max_ctx, HY_KV_BLOCK_TOKENS));
+  const int bps = ceil_div(max_blocks, ns);
+  ns = ceil_div(max_blocks, bps);
+  dim3 grid(n, n_kv_heads, ns);
+  const float sl2 = scale * 1.4426950408889634f;
+  const bf16* qp = reinterpret_cast<const bf16*>(q);
+  const bf16* kvp = reinterpret_cast<const bf16*>(kv_layer);
+  bf16* op = reinterpret_cast<bf16*>(out);
+  float* part = reinterpret_cast<float*>(workspace);
+#define HY_DEC_CASE(GG)                                                                        \
+  case GG:                                                                                     \
+    attn_decode_kernel<GG><<<grid, 128, 0, stream>>>(qp, ld_q, n_kv_heads, slots, ctx,         \
+                                                     block_table, bt_stride, kvp, block_stride, \
+                                                     sl2, bps, op, ld_o, part, ns);            \
+    break;
+  switch (G) {
+    HY_DEC_CASE(1)
+    HY_DEC_CASE(2)
+    HY_DEC_CASE(4)
+    HY_DEC_CASE(7)
+    HY_DEC_CASE(8)
+    default:
+      set_last_error("decode attention: unsupported GQA group " + std::to_string(G));
+      return (int)cudaErrorInvalidValue;
+  }
+#undef HY_DEC_CASE
+  HY_LAUNCH_CHECK();
+  if (ns > 1) {
+    attn_decode_combine_kernel<<<dim3(n, n_heads), 128, 0, stream>>>(part, n_heads, ns, op, ld_o);
+    HY_LAUNCH_CHECK();
+  }
+  return 0;
+}
