@@ -1,0 +1,462 @@
+#!/usr/bin/env python
+"""bench.py -- HydraInfer serving hot path on B200 (BASELINE.json metric).
+
+Metric: req/s at P90 TTFT+TPOT SLO (SLO attainment >= 0.9, metrics.py:57-68,214-262),
+with decode tok/s and KV-migration GB/s reported beside it.
+
+Workload (N=1): BASELINE config 2 -- LLaVA-1.5-7B shape (CLIP ViT-L/14-336 + Llama-2-7B,
+random-init bf16), colocated EPD:1 on one B200, TextCaps-shaped synthetic trace
+``synth_trace(seed=7, 1 image x 576 tokens, prompt {25,35,45}, output {90,110,130})``
+(SURVEY.md 8d config 4 shape), SLO (4.0 s, 0.08 s).  With --gpus N (torchrun) every rank
+runs its own EPD:1 replica on its round-robin share of an N-times longer trace: requests
+are independent units, so this is weak scaling with no data-path collective.
+
+One "step" = one goodput probe: a full replay of the trace, scaled to the probe rate,
+through the reference scheduler (epdsim) with every batch executed on the GPU and the
+virtual clock advanced by each batch's CUDA-event time (inputs resident in HBM).  K steps
+= K geometric-bisection probes of ``find_goodput`` (metrics.py:214-262); W warm-up
+replays precede them.  ``value`` = the largest probed rate with attainment >= 0.9.
+
+e2e: the same metric through the same public API with the images copied from pinned host
+memory every batch, the new tokens read back every batch, and each batch's latency the
+host wall time of the whole call (probed at the found rate and below).
+
+--impl reference: the reference's own implementation of the path -- epdsim's analytic
+executor (batch_latency / transfer_seconds, 1 host core) -- searched the same way on the
+same trace with a B200 HardwareProfile built from MEASURED_PEAKS.json.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "req/s at P90 TTFT+TPOT SLO on 8×B200; decode tok/s; KV-migration GB/s"
+UNIT = "req/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=6, help="goodput bisection probes")
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="llava-1.5-7b")
+    ap.add_argument("--method", default="EPD:1")
+    ap.add_argument("--requests", type=int, default=600, help="trace requests per GPU")
+    ap.add_argument("--rate-lo", type=float, default=4.0, help="per-GPU req/s")
+    ap.add_argument("--rate-hi", type=float, default=160.0, help="per-GPU req/s")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+def base_trace(E, n, seed=7):
+    slo = E.SloSpec(4.0, 0.08)
+    return E.synth_trace(seed=seed, n_requests=n, rate=1.0, image_count_dist=1,
+                         visual_token_choices=576, prompt_dist=[25, 35, 45],
+                         output_dist=[90, 110, 130], slo=slo, name="textcaps_synth"), slo
+
+
+def shard(E, trace, rank, world):
+    return E.Trace(tuple(r for i, r in enumerate(trace.requests) if i % world == rank),
+                   name=trace.name)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s, p in zip(sm, power) if p > 300] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm), "samples_under_load": len(loaded),
+                "power_w_max": max(power) if power else None}
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")  # scalar metrics only; no data-path collective
+            self.dist = dist
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def reduce(self, values, op="sum"):
+        if self.world == 1:
+            return values
+        import torch
+        t = torch.tensor(values, dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM if op == "sum" else self.dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def geometric_bisect(probe, lo, hi, steps, threshold=0.9):
+    """find_goodput (metrics.py:214-262) with a geometric midpoint and a fixed probe
+    count; returns (rate, probes).  Every probe is one timed step."""
+    probes = []
+    best = None
+    for _ in range(steps):
+        mid = math.sqrt(lo * hi)
+        att = probe(mid)
+        probes.append((mid, att))
+        if att >= threshold:
+            lo, best = mid, mid
+        else:
+            hi = mid
+    return best, probes
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args, d: Dist):
+    import torch
+    import paper_2505_12658_b200 as P
+    from paper_2505_12658_b200 import _lib
+    from paper_2505_12658_b200._epdsim import C, E
+    from paper_2505_12658_b200.cluster import GpuCluster
+    from paper_2505_12658_b200.profiling import KernelSampler
+    from paper_2505_12658_b200.weights import DeviceWeights
+
+    torch.cuda.set_device(d.local)
+    dev = torch.device("cuda", d.local)
+    peaks, peak_src = measured_peaks()
+    shape = P.get_shape(args.model)
+    hw = P.b200_hardware()
+    spec = C.ClusterSpec(method=C.DisaggregationMethod.parse(args.method))
+    lib = _lib.load()
+    weights = {dev: DeviceWeights(shape, dev, args.seed)}
+    base, slo = base_trace(E, args.requests * d.world)
+    my = shard(E, base, d.rank, d.world)
+    sampler = KernelSampler(dev, every=4)
+
+    def replay(rate_total, clock="device", resident=True, sample=False, trace=None):
+        tr = E.scale_to_rate(trace or base, rate_total)
+        tr = shard(E, tr, d.rank, d.world) if trace is None else tr
+        cl = GpuCluster(spec, shape, hw, slo, devices=[dev], clock=clock, seed=args.seed,
+                        resident_inputs=resident, weights=weights)
+        if sample:
+            for rt in cl.runtimes.values():
+                rt.sampler = sampler
+        rep = cl.run(tr)
+        return cl, rep
+
+    # ---- warm-up (untimed): short replays exercise every kernel shape class
+    warm = E.Trace(base.requests[:24], name="warm")
+    for i in range(args.warmup):
+        replay(50.0 * (i + 1), trace=warm)
+    torch.cuda.synchronize()
+
+    # ---- timed goodput search: K probes
+    probe_info = []
+    clocks = ClockSampler(d.local)
+    launches0 = lib.hy_launch_count()
+    d.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t_all0 = time.perf_counter()
+
+    def probe(rate_per_gpu):
+        total = rate_per_gpu * d.world
+        d.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cl, rep = replay(total, sample=True)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        a = rep.aggregates
+        meets = sum(1 for m in rep.requests if P.epdsim.meets_slo(m))
+        tot = d.reduce([meets, len(rep.requests), a["n_finished"],
+                        sum(r.tokens_out for r in cl.reqs.values()),
+                        sum(rt.stats["device_ms"] for rt in cl.runtimes.values()),
+                        sum(rt.stats["batches"] for rt in cl.runtimes.values())])
+        span = d.reduce([max(s.t_done for s in cl.reqs.values()) -
+                         min(s.spec.arrival_time for s in cl.reqs.values()), dt], op="max")
+        att = tot[0] / tot[1]
+        probe_info.append({"rate": total, "attainment": att, "wall_s": span[1],
+                           "virtual_span_s": span[0], "tokens": tot[3],
+                           "decode_tok_s": tot[3] / span[0] if span[0] > 0 else 0.0,
+                           "device_busy_s": tot[4] / 1e3, "batches": int(tot[5]),
+                           "ttft_p90": a["ttft_percentiles_s"].get("p90"),
+                           "tbt_p90": a["tbt_percentiles_s"].get("p90")})
+        return att
+
+    best, probes = geometric_bisect(probe, args.rate_lo, args.rate_hi, args.steps)
+    torch.cuda.synchronize()
+    d.barrier()
+    t_all = d.reduce([time.perf_counter() - t_all0], op="max")[0]
+    clk = clocks.stop()
+    launches = int(d.reduce([lib.hy_launch_count() - launches0])[0])
+    value = (best or 0.0) * d.world
+    best_probe = max((p for p in probe_info if p["attainment"] >= 0.9),
+                     key=lambda p: p["rate"], default=None)
+
+    # ---- roofline of the dominant kernel, timed live inside the probes
+    summ = sampler.summary()
+    dominant = max(summ, key=lambda k: summ[k]["share_of_batch_time"]) if summ else None
+
+    def roof(name):
+        s = summ[name]
+        if name == "decode_attn":
+            ach = s["work_per_ms"] / 1e6  # bytes/ms -> GB/s
+            return {"kernel": "attn_decode_kernel (K8)", "bound": "hbm", "achieved": ach,
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
+                    "traffic": traffic_of("decode_attn"), "launches_timed": s["launches"],
+                    "avg_launch_ms": s["avg_ms"], "share_of_step": s["share_of_batch_time"],
+                    "peak_source": f"{peak_src} hbm_gbs"}
+        ach = s["work_per_ms"] / 1e9  # flop/ms -> TFLOP/s
+        pk = peaks["bf16_tflops_sustained"]
+        return {"kernel": {"gemm": "gemm_tc_kernel (K1, tcgen05)",
+                           "prefill_attn": "attn_fa2_kernel<128,paged> (K7)",
+                           "vit_attn": "attn_fa2_kernel<64> (K3)"}[name],
+                "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                "frac": ach / pk, "traffic": traffic_of(name), "launches_timed": s["launches"],
+                "avg_launch_ms": s["avg_ms"], "share_of_step": s["share_of_batch_time"],
+                "peak_source": f"{peak_src} bf16_tflops_sustained"}
+
+    def traffic_of(name):
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                return json.load(fh).get(name)
+        except OSError:
+            return None
+
+    roofline = roof(dominant) if dominant else None
+    others = {k: roof(k) for k in summ if k != dominant}
+
+    # ---- end-to-end through host buffers (wall clock per batch)
+    e2e = None
+    if not args.no_e2e and best:
+        e2e_rate = None
+        e2e_probes = []
+        img_bytes = shape.patch_grid(576)[0] * shape.patch_grid(576)[1] * shape.patch ** 2 * 3
+        for f in (1.0, 0.85, 0.7, 0.5):
+            r = best * f
+            cl, rep = replay(r * d.world, clock="wall", resident=False)
+            meets = sum(1 for m in rep.requests if P.epdsim.meets_slo(m))
+            tot = d.reduce([meets, len(rep.requests)])
+            att = tot[0] / tot[1]
+            e2e_probes.append((r * d.world, att))
+            if att >= 0.9:
+                e2e_rate = r * d.world
+                n_img = sum(rt.stats["images"] for rt in cl.runtimes.values())
+                n_tok = sum(r_.tokens_out for r_ in cl.reqs.values())
+                break
+        e2e = {"value": e2e_rate or 0.0, "unit": UNIT,
+               "h2d_bytes_per_step": None, "d2h_bytes_per_step": None, "probes": e2e_probes,
+               "clock": "host wall time per batch (lowering + H2D pixels + GPU + D2H tokens)"}
+        if e2e_rate:
+            # a step is one replay; bytes are this replay's per-GPU pixel uploads and
+            # token read-backs (int32 per generated token)
+            e2e["h2d_bytes_per_step"] = n_img * img_bytes
+            e2e["d2h_bytes_per_step"] = n_tok * 4
+
+    # ---- CPU baseline: the oracle port on the host cores (bounded sample)
+    cpu = None
+    if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(shape)
+
+    if d.rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_all * 1e3 / max(1, args.steps), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, synthetic pixels/prompt ids)",
+            "config": {"workload": f"{args.model} shape, {args.method} per GPU, TextCaps-shaped "
+                                   "synth_trace(seed=7): 1 image x 576 tokens, prompt {25,35,45}, "
+                                   "output {90,110,130}; SLO TTFT 4 s / TBT 0.08 s",
+                       "model": args.model, "method": args.method,
+                       "requests_per_gpu": args.requests,
+                       "rate_bounds_per_gpu": [args.rate_lo, args.rate_hi],
+                       "parallelism": f"dp{d.world} (independent EPD replicas)",
+                       "l2": "inputs larger than L2: 14 GB weights + paged KV streamed per step",
+                       "clock": "virtual clock advanced by CUDA-event time of each batch"},
+            "decode_tok_s": best_probe["decode_tok_s"] if best_probe else 0.0,
+            "kv_migration_gbs": None,
+            "probes": probe_info,
+            "roofline": roofline, "roofline_other_kernels": others,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        }
+        print(json.dumps(line))
+
+
+def cpu_baseline(shape):
+    """fp32 CPU oracle on a bounded sample of the same workload, all host cores."""
+    import torch
+    from oracle.mllm_fp32 import OracleMLLM
+    from paper_2505_12658_b200 import with_layers
+    from paper_2505_12658_b200.inputs import ImageStore, prompt_tokens
+    from paper_2505_12658_b200.weights import weight_specs
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    sample = with_layers(shape, n_layers=2, v_layers=2)
+    o = OracleMLLM.random_for_timing(sample.asdict(), weight_specs(sample))
+    gh, gw = shape.patch_grid(576)
+    px = ImageStore(0, shape.patch).request_image("r0", 0, gh, gw)
+    prompt = prompt_tokens(0, "r0", 35, shape.vocab)
+    t0 = time.perf_counter()
+    o.add_image_rows("r0", o.encode_image(px, gh, gw))
+    t_enc = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    lg = o.prefill_chunk("r0", prompt, 576, 0, 576 + 35)
+    t_pf = time.perf_counter() - t0
+    tok = int(lg.argmax())
+    steps = 8
+    t0 = time.perf_counter()
+    for i in range(steps):
+        tok = int(o.decode("r0", tok, 611 + i).argmax())
+    t_dec = (time.perf_counter() - t0) / steps
+    # scale the sampled layers to the full depth (lm_head counted once per sampled run)
+    lf = shape.n_layers / sample.n_layers
+    vf = shape.v_layers / sample.v_layers
+    t_req = t_enc * vf + t_pf * lf + 109 * t_dec * lf
+    return {"value": 1.0 / t_req, "unit": "req/s (one request, no batching, no SLO)",
+            "cores": cores, "kind": "port",
+            "sample": (f"oracle/mllm_fp32 on {sample.n_layers}/{shape.n_layers} LLM and "
+                       f"{sample.v_layers}/{shape.v_layers} ViT layers of {shape.name}: 1 image "
+                       "encode + 611-token prefill + 8 decode steps, times scaled by depth to a "
+                       "110-token request"),
+            "decode_tok_s": 1.0 / (t_dec * lf), "ttft_s": t_enc * vf + t_pf * lf,
+            "slo_attainment": 0.0 if t_enc * vf + t_pf * lf > 4.0 else None}
+
+
+# ----------------------------------------------------------------------------- reference
+def run_reference(args, d: Dist):
+    if d.rank != 0:
+        return
+    from paper_2505_12658_b200._epdsim import C, E
+    peaks, src = measured_peaks()
+    hw = E.HardwareProfile(peaks["bf16_tflops_sustained"] * 1e12, peaks["hbm_gbs"] * 1e9,
+                           160e9, 14e9, 770e9)
+    model = E.MODEL_PRESETS[args.model] if args.model in E.MODEL_PRESETS else None
+    spec = C.ClusterSpec(method=C.DisaggregationMethod.parse(args.method))
+    base, slo = base_trace(E, args.requests * args.gpus)
+    warm = E.Trace(base.requests[:24], name="warm")
+    for i in range(args.warmup):
+        C.run_trace(spec, model, hw, slo, E.scale_to_rate(warm, 50.0 * (i + 1)))
+    probes = []
+
+    def probe(rate_per_gpu):
+        tr = E.scale_to_rate(base, rate_per_gpu * args.gpus)
+        # N GPUs = N independent replicas, each on its shard
+        meets = total = 0
+        for rank in range(args.gpus):
+            rep = C.run_trace(spec, model, hw, slo, shard(E, tr, rank, args.gpus))
+            meets += sum(1 for m in rep.requests if E.meets_slo(m))
+            total += len(rep.requests)
+        probes.append((rate_per_gpu * args.gpus, meets / total,
+                       rep.aggregates["token_throughput_tps"]))
+        return meets / total
+
+    t0 = time.perf_counter()
+    best, _ = geometric_bisect(probe, args.rate_lo, args.rate_hi, args.steps)
+    dt = time.perf_counter() - t0
+    value = (best or 0.0) * args.gpus
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.model}, {args.method} per GPU, same trace/SLO as ours",
+                       "executor": "epdsim analytic roofline (batch_latency, transfer_seconds) "
+                                   f"with a B200 HardwareProfile from {src} peaks"},
+            "probes": probes,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                             "sample": f"epdsim find_goodput-style search, {args.steps} replays "
+                                       f"of {args.requests * args.gpus} requests, 1 host core"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    d = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, d)
+        else:
+            run_ours(args, d)
+    finally:
+        d.close()
+
+
+if __name__ == "__main__":
+    main()

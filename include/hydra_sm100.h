@@ -69,6 +69,25 @@ typedef struct HyGemmEpilogue {
 const char* hy_last_error(void);
 int hy_version(void);
 int hy_device_sm_count(void);
+/* total kernels launched by this library in this process */
+long long hy_launch_count(void);
+
+/* Live per-kernel timing: while a timer is installed, the composite forwards record a
+ * (begin, end) cudaEvent pair around every launch of kernel class `klass` on the
+ * launching stream, and the launch's algorithmic work (GEMM: 2MNK flops; attention: 0,
+ * filled by the caller) into work[i].  events: host array of 2*capacity cudaEvent_t. */
+#define HY_KCLASS_DECODE_ATTN 1
+#define HY_KCLASS_GEMM 2
+#define HY_KCLASS_PREFILL_ATTN 3
+#define HY_KCLASS_VIT_ATTN 4
+typedef struct HyKernelTimer {
+  int klass;
+  int capacity;
+  int count;
+  void* events;  /* cudaEvent_t[2 * capacity] */
+  double* work;  /* [capacity] or NULL */
+} HyKernelTimer;
+void hy_set_kernel_timer(HyKernelTimer* timer);
 
 /* ---------------- K1: GEMM (tcgen05 + TMEM + TMA) ---------------- */
 /* out = epi(A[M,K] . W[N,K]^T).  K, lda, ldw % 8 == 0, N % 16 == 0.

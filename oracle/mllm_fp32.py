@@ -68,6 +68,22 @@ class OracleMLLM:
         self.kv: Dict[str, List[Tuple[torch.Tensor, torch.Tensor]]] = {}
         self.image_rows: Dict[str, torch.Tensor] = {}
 
+    @classmethod
+    def random_for_timing(cls, shape: Dict, specs: Sequence, seed: int = 0) -> "OracleMLLM":
+        """Same architecture with torch-random weights (fast to build); used only to time
+        the CPU baseline, never as a parity reference."""
+        o = cls.__new__(cls)
+        o.s = dict(shape)
+        o.seed = seed
+        g = torch.Generator().manual_seed(seed)
+        o.w = {}
+        for sp in specs:
+            t = (torch.rand(sp.rows, sp.cols, generator=g) * 2 - 1) * sp.scale + sp.offset
+            o.w[sp.name] = t[0] if sp.rows == 1 else t
+        o.kv = {}
+        o.image_rows = {}
+        return o
+
     # ------------------------------------------------------------------ vision
     def im2col(self, pixels: np.ndarray, gh: int, gw: int) -> torch.Tensor:
         p = self.s["patch"]

@@ -83,6 +83,17 @@ class HyVitModel(Structure):
                 ("b_proj1", c_void_p), ("w_proj2", c_void_p), ("b_proj2", c_void_p)]
 
 
+class HyKernelTimer(Structure):
+    _fields_ = [("klass", c_int), ("capacity", c_int), ("count", c_int), ("events", c_void_p),
+                ("work", c_void_p)]
+
+
+HY_KCLASS_DECODE_ATTN = 1
+HY_KCLASS_GEMM = 2
+HY_KCLASS_PREFILL_ATTN = 3
+HY_KCLASS_VIT_ATTN = 4
+
+
 class HyVitBatch(Structure):
     _fields_ = [("n_images", c_int), ("n_tokens", c_int), ("n_patches", c_int),
                 ("n_visual", c_int), ("max_image_tokens", c_int), ("images", c_void_p),
@@ -94,6 +105,8 @@ _SIGS = {
     "hy_last_error": (c_char_p, []),
     "hy_version": (c_int, []),
     "hy_device_sm_count": (c_int, []),
+    "hy_launch_count": (c_longlong, []),
+    "hy_set_kernel_timer": (None, [c_void_p]),
     "hy_gemm_bf16": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int,
                              POINTER(HyGemmEpilogue), c_void_p, c_size_t, c_void_p]),
     "hy_gemm_bf16_mode": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int,

@@ -59,12 +59,15 @@ class GpuCluster(C.Cluster):
                  probe_image_tokens: int = MC.IMAGE_BLOCK_TOKENS, max_slots: int = 4096,
                  max_seq_tokens: int = 16384, record_batches: bool = False,
                  weights: Optional[Dict] = None, capture: bool = False,
-                 pool_bytes_limit: Optional[int] = None):
+                 pool_bytes_limit: Optional[int] = None, profile_override=None):
         if clock not in CLOCKS:
             raise ValueError(f"clock must be one of {CLOCKS}")
         if not torch.cuda.is_available():
             raise RuntimeError("GpuCluster needs a CUDA device (there is no CPU fallback)")
-        super().__init__(spec, shape.profile(), hw, slo, probe_image_tokens)
+        # the scheduler normally sees exactly the executed shape; parity tests that run a
+        # depth-reduced model under the full model's decisions pass the full profile
+        profile = profile_override if profile_override is not None else shape.profile()
+        super().__init__(spec, profile, hw, slo, probe_image_tokens)
         self.shape = shape
         self.clock = clock
         self.seed = seed
@@ -183,8 +186,14 @@ class GpuCluster(C.Cluster):
 
     def run(self, trace, check_invariants: bool = False):
         report = super().run(trace, check_invariants=check_invariants)
+        merged: Dict[str, List] = {}
         for rt in self.runtimes.values():
-            rt.collect_tokens(self.generated)
+            rt.collect_tokens(rt.generated)
+            for rid, toks in rt.generated.items():
+                merged.setdefault(rid, []).extend(toks)
+            rt.generated.clear()
+        for rid, toks in merged.items():
+            self.generated[rid] = [t for _, t in sorted(toks)]
         return report
 
     def _assert_invariants(self) -> None:

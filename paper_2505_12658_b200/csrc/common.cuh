@@ -38,8 +38,11 @@ const char* get_last_error();
     }                                                                        \
   } while (0)
 
+void count_launch();
+
 #define HY_LAUNCH_CHECK()                                                    \
   do {                                                                       \
+    ::hy::count_launch();                                                    \
     cudaError_t e__ = cudaGetLastError();                                    \
     if (e__ != cudaSuccess) {                                                \
       ::hy::set_last_error(std::string("launch failed at ") + __FILE__ + ":" + \
@@ -239,5 +242,8 @@ int make_tmap_2d_bf16(CUtensorMap* tm, const void* base, uint64_t rows, uint64_t
                       uint64_t row_stride_bytes, uint32_t box_rows, uint32_t box_cols);
 
 int num_sms();
+
+// kernel-class timer hooks (see hy_set_kernel_timer)
+void timer_mark(int klass, cudaStream_t st, bool begin, double work);
 
 }  // namespace hy

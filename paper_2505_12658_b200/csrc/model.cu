@@ -104,8 +104,11 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
     e.out = out;
     e.ldc = ldc;
     e.out_f32 = f32;
-    return gemm_bf16(A, lda, reinterpret_cast<const bf16*>(W), K, M, N, K, &e, w.gemm_ws, kGemmWs,
-                     st, 0);
+    timer_mark(HY_KCLASS_GEMM, st, true, 0.0);
+    int rc = gemm_bf16(A, lda, reinterpret_cast<const bf16*>(W), K, M, N, K, &e, w.gemm_ws,
+                       kGemmWs, st, 0);
+    timer_mark(HY_KCLASS_GEMM, st, false, 2.0 * M * N * K);
+    return rc;
   };
   const float scale = 1.0f / sqrtf((float)D);
   HY_RET_IF(hy_merge_embed(b->tok, R, m->embed, image_rows, H, last_tok, b->row_slot, w.x, st));
@@ -121,17 +124,21 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
                                 b->row_slot, kv->block_table, kv->bt_stride, kv_layer,
                                 kv->block_stride, m->rope_theta, st));
     if (nd > 0) {
+      timer_mark(HY_KCLASS_DECODE_ATTN, st, true, 0.0);
       HY_RET_IF(hy_attn_decode_paged(w.qkv, qkv_cols, nd, m->n_heads, m->n_kv_heads, D,
                                      b->row_slot, b->dec_ctx, b->max_ctx, kv->block_table,
                                      kv->bt_stride, kv_layer, kv->block_stride, scale, w.attn, QD,
                                      w.dec_ws, w.dec_ws_bytes, st));
+      timer_mark(HY_KCLASS_DECODE_ATTN, st, false, 0.0);
     }
     if (b->n_prefill > 0 && np_rows > 0) {
+      timer_mark(HY_KCLASS_PREFILL_ATTN, st, true, 0.0);
       HY_RET_IF(hy_attn_prefill_paged(w.qkv + (size_t)nd * qkv_cols, qkv_cols, b->n_prefill,
                                       b->pf_qstart, b->pf_offset, b->pf_slot, b->pf_max_q,
                                       m->n_heads, m->n_kv_heads, D, kv->block_table,
                                       kv->bt_stride, kv_layer, kv->block_stride, scale,
                                       w.attn + (size_t)nd * QD, QD, st));
+      timer_mark(HY_KCLASS_PREFILL_ATTN, st, false, 0.0);
     }
     HY_RET_IF(G(w.attn, QD, L.w_o, R, H, QD, nullptr, w.x, H, HY_ACT_NONE, w.x, H, 0));
     HY_RET_IF(rmsnorm(w.x, H, L.ffn_norm, w.t, H, R, H, m->rms_eps, nullptr, st));
@@ -205,8 +212,11 @@ extern "C" int hy_vit_forward(const HyVitModel* m, const HyVitBatch* b, void* wo
     e.row_map = row_map;
     e.out = out;
     e.ldc = ldc;
-    return gemm_bf16(A, lda, reinterpret_cast<const bf16*>(W), K, M, N, K, &e, w.gemm_ws, kGemmWs,
-                     st, 0);
+    timer_mark(HY_KCLASS_GEMM, st, true, 0.0);
+    int rc = gemm_bf16(A, lda, reinterpret_cast<const bf16*>(W), K, M, N, K, &e, w.gemm_ws,
+                       kGemmWs, st, 0);
+    timer_mark(HY_KCLASS_GEMM, st, false, 2.0 * M * N * K);
+    return rc;
   };
   // K2: patch embedding
   HY_RET_IF(hy_im2col_patches(b->images, b->n_images, b->n_patches, m->patch, m->merge, m->k_pad,
@@ -222,8 +232,10 @@ extern "C" int hy_vit_forward(const HyVitModel* m, const HyVitBatch* b, void* wo
     HY_RET_IF(layernorm(w.h, Hv, L.ln1_w, L.ln1_b, w.t, Hv, T, Hv, m->ln_eps, nullptr, st));
     HY_RET_IF(G(w.t, Hv, L.w_qkv, T, 3 * Hv, Hv, L.b_qkv, nullptr, 0, HY_ACT_NONE, w.qkv, 3 * Hv,
                 nullptr));
+    timer_mark(HY_KCLASS_VIT_ATTN, st, true, 0.0);
     HY_RET_IF(hy_attn_varlen(w.qkv, 3 * Hv, b->n_images, b->seg, b->max_image_tokens, m->n_heads,
                              m->head_dim, scale, w.a, Hv, st));
+    timer_mark(HY_KCLASS_VIT_ATTN, st, false, 0.0);
     HY_RET_IF(G(w.a, Hv, L.w_o, T, Hv, Hv, L.b_o, w.h, Hv, HY_ACT_NONE, w.h, Hv, nullptr));
     HY_RET_IF(layernorm(w.h, Hv, L.ln2_w, L.ln2_b, w.t, Hv, T, Hv, m->ln_eps, nullptr, st));
     HY_RET_IF(G(w.t, Hv, L.w_fc1, T, m->mlp, Hv, L.b_fc1, nullptr, 0, HY_ACT_QUICK_GELU, w.f,

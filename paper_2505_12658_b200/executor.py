@@ -26,6 +26,7 @@ It never mutates ``batch`` or ``reqs`` (the loop does that in ``_on_batch_done``
 
 from __future__ import annotations
 
+import itertools
 import time
 from typing import Dict, List, Optional, Tuple
 
@@ -42,6 +43,7 @@ from .weights import DeviceWeights
 IMG = MC.IMAGE_BLOCK_TOKENS
 KVB = MC.KV_BLOCK_TOKENS
 CLOCKS = ("oracle", "device", "wall")
+_BATCH_SEQ = itertools.count()  # global batch order, to merge tokens across instances
 
 
 class _Staging:
@@ -121,11 +123,13 @@ class InstanceRuntime:
         self._prompts: Dict[str, np.ndarray] = {}
         self.tok_cursor = 0
         self.tok_records: List[Tuple[int, List[str]]] = []
+        self.generated: Dict[str, List[int]] = {}
         self.launches = 0
         # parity capture: per batch, the pre-batch cursors and the logits of every row
         # that emits a token (tests only; costs a D2H per batch)
         self.capture = capture
         self.exec_log: List[Dict] = []
+        self.sampler = None  # profiling.KernelSampler (bench.py)
         self.stats = {"batches": 0, "lang_rows": 0, "decode_rows": 0, "prefill_rows": 0,
                       "images": 0, "device_ms": 0.0, "host_ms": 0.0}
 
@@ -319,6 +323,9 @@ class InstanceRuntime:
         self.ev_start.record(sl)
         sv.wait_event(self.ev_start)
         self.sync_block_tables(sl)
+        sampler = self.sampler
+        if sampler is not None:
+            sampler.before_batch()
         has_lang = bool(batch.decode_entries or batch.prefill_chunks)
         has_vis = bool(batch.encode_entries)
         out_rids: List[str] = []
@@ -330,8 +337,8 @@ class InstanceRuntime:
             self._ensure_lang_ws(n_rows, n_out, nd, max_ctx)
             ptrs = self._upload(self.meta, parts, sl)
             if self.tok_cursor + n_out > self.tok_log.numel():
-                self.tok_cursor = 0
-                self.tok_records.clear()
+                torch.cuda.synchronize(dev)
+                self.collect_tokens(self.generated)  # drain the device token log
             tok_off = self.tok_cursor
             out_tok_ptr = self.tok_log.data_ptr() + 4 * tok_off
             logits_ptr = 0
@@ -355,7 +362,7 @@ class InstanceRuntime:
         self.ev_l.record(sl)
         self.ev_v.record(sv)
         if n_out:
-            self.tok_records.append((tok_off, out_rids))
+            self.tok_records.append((tok_off, out_rids, next(_BATCH_SEQ)))
             self.tok_cursor += n_out
         if clock == "wall" and n_out:
             # end-to-end: read this step's tokens back to the host
@@ -367,6 +374,10 @@ class InstanceRuntime:
         dev_ms = max(self.ev_start.elapsed_time(self.ev_l),
                      self.ev_start.elapsed_time(self.ev_v) if has_vis else 0.0)
         host_s = time.perf_counter() - t_host0
+        if sampler is not None:
+            ctx_sum = sum(kl + 1 for _, kl in batch.decode_entries)
+            sampler.after_batch(dev_ms, ctx_sum * self.shape.kv_bytes_per_token /
+                                self.shape.n_layers)
         self.stats["batches"] += 1
         if self.capture:
             entry = {
@@ -464,8 +475,8 @@ class InstanceRuntime:
         if not self.tok_records:
             return
         host = self.tok_log[:self.tok_cursor].cpu().numpy()
-        for off, rids in self.tok_records:
+        for off, rids, seq in self.tok_records:
             for j, rid in enumerate(rids):
-                out.setdefault(rid, []).append(int(host[off + j]))
+                out.setdefault(rid, []).append((seq, int(host[off + j])))
         self.tok_records.clear()
         self.tok_cursor = 0

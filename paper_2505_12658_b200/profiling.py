@@ -1,0 +1,91 @@
+"""Live kernel timing inside the serving loop (for bench.py's roofline numbers).
+
+``KernelSampler`` installs a ``HyKernelTimer`` (include/hydra_sm100.h) on a sample of
+batches: the native forward brackets every launch of the chosen kernel class with a
+CUDA event pair on the launching stream, so the kernel's duration is measured where it
+actually runs -- inside the timed serving region, not in a separate microbenchmark.
+
+Algorithmic work per launch:
+  GEMM           2*M*N*K flops (recorded by the library)
+  decode attn    bytes = sum_i ctx_i * kv_bytes_per_token_per_layer (K+V of every key
+                 read once; epdsim charges 2*B*H*(S+1)*ratio per layer,
+                 model_cost.py:195) -- filled in here from the batch
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, List
+
+import torch
+
+from . import _lib
+
+
+class KernelSampler:
+    CLASSES = {"gemm": _lib.HY_KCLASS_GEMM, "decode_attn": _lib.HY_KCLASS_DECODE_ATTN,
+               "prefill_attn": _lib.HY_KCLASS_PREFILL_ATTN, "vit_attn": _lib.HY_KCLASS_VIT_ATTN}
+
+    def __init__(self, device, every: int = 8, capacity: int = 512):
+        self.every = every
+        self.capacity = capacity
+        self.lib = _lib.load()
+        with torch.cuda.device(device):
+            self.events = [torch.cuda.Event(enable_timing=True) for _ in range(2 * capacity)]
+            s = torch.cuda.current_stream(device)
+            for e in self.events:
+                e.record(s)  # materialise the cudaEvent_t handles
+            s.synchronize()
+        self._handles = (ctypes.c_void_p * (2 * capacity))(*[e.cuda_event for e in self.events])
+        self._work = (ctypes.c_double * capacity)()
+        self.timer = _lib.HyKernelTimer(0, capacity, 0, ctypes.addressof(self._handles),
+                                        ctypes.addressof(self._work))
+        self.n_batches = 0
+        self.active = None
+        # per class: list of (ms, work) per launch; plus sampled batch device time
+        self.samples: Dict[str, List] = {k: [] for k in self.CLASSES}
+        self.batch_ms: Dict[str, float] = {k: 0.0 for k in self.CLASSES}
+        self.class_ms: Dict[str, float] = {k: 0.0 for k in self.CLASSES}
+        self.order = list(self.CLASSES)
+
+    def before_batch(self) -> None:
+        self.n_batches += 1
+        self.active = None
+        if self.n_batches % self.every:
+            return
+        name = self.order[(self.n_batches // self.every) % len(self.order)]
+        self.active = name
+        self.timer.klass = self.CLASSES[name]
+        self.timer.count = 0
+        self.lib.hy_set_kernel_timer(ctypes.byref(self.timer))
+
+    def after_batch(self, batch_device_ms: float, decode_ctx_bytes: float) -> None:
+        """Call after the batch completed (events are final)."""
+        if self.active is None:
+            return
+        self.lib.hy_set_kernel_timer(None)
+        name = self.active
+        tot = 0.0
+        for i in range(self.timer.count):
+            ms = self.events[2 * i].elapsed_time(self.events[2 * i + 1])
+            work = self._work[i]
+            if name == "decode_attn":
+                work = decode_ctx_bytes
+            self.samples[name].append((ms, work))
+            tot += ms
+        self.batch_ms[name] += batch_device_ms
+        self.class_ms[name] += tot
+        self.active = None
+
+    def summary(self) -> Dict[str, Dict]:
+        out = {}
+        for name, s in self.samples.items():
+            if not s:
+                continue
+            ms = sum(x for x, _ in s)
+            work = sum(w for _, w in s)
+            out[name] = {"launches": len(s), "avg_ms": ms / len(s), "total_ms": ms,
+                         "work": work, "work_per_ms": work / ms if ms > 0 else 0.0,
+                         "share_of_batch_time": (self.class_ms[name] / self.batch_ms[name]
+                                                 if self.batch_ms[name] > 0 else 0.0)}
+        return out

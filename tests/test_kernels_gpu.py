@@ -1,0 +1,346 @@
+"""Per-kernel parity on the GPU through the C ABI.
+
+Byte/integer kernels (weight synthesis, block copy, merge gather, argmax, block-table
+scatter) must be bit-exact against the oracle; floating-point kernels are checked
+against a plain PyTorch fp32 reference of the same op with the tolerance written in each
+test (bf16 storage, fp32 accumulation).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2505_12658_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def lib():
+    return _lib.load()
+
+
+def st():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ck(rc, what=""):
+    _lib.check(rc, what)
+
+
+# ---------------------------------------------------------------- synthesis
+@pytest.mark.parametrize("rows,cols,ld,perm", [(7, 33, 40, 0), (64, 48, 48, 1), (1, 4096, 4096, 0)])
+def test_fill_uniform_bit_exact(rows, cols, ld, perm):
+    from oracle.synth import swiglu_physical_rows, uniform_tensor
+    t = torch.empty(rows, ld, dtype=torch.bfloat16, device=DEV)
+    ck(lib().hy_fill_uniform_bf16(t.data_ptr(), rows, cols, ld, 11, 99, 0.035, 0.5, perm, st()))
+    got = t.float().cpu().numpy()
+    ref = uniform_tensor(11, 99, rows, cols, 0.035, 0.5)
+    if perm == 1:
+        ref = ref[swiglu_physical_rows(rows)]
+    assert np.array_equal(got[:, :cols], ref)
+    assert np.all(got[:, cols:] == 0)
+
+
+# ---------------------------------------------------------------- GEMM
+def _gemm_ref(A, W, bias, act, res):
+    y = A.float() @ W.float().T
+    if bias is not None:
+        y = y + bias.float()
+    if act == _lib.HY_ACT_SWIGLU:
+        M, N = y.shape
+        g = y.view(M, N // 32, 2, 16)
+        y = (torch.nn.functional.silu(g[:, :, 0]) * g[:, :, 1]).reshape(M, N // 2)
+    elif act == _lib.HY_ACT_QUICK_GELU:
+        y = y * torch.sigmoid(1.702 * y)
+    elif act == _lib.HY_ACT_GELU:
+        y = torch.nn.functional.gelu(y)
+    if res is not None:
+        y = y + res.float()
+    return y
+
+
+@pytest.mark.parametrize("M,N,K,mode,act,bias,res,f32", [
+    (1, 4096, 4096, 0, 0, False, False, False),      # decode: swap-AB + split-K
+    (7, 12288, 512, 0, 0, False, True, False),
+    (33, 1536, 512, 0, 4, False, False, False),       # swap-AB + SwiGLU (shuffle pairing)
+    (64, 2816, 512, 1, 4, False, False, False),
+    (200, 1024, 1024, 0, 2, True, True, False),
+    (256, 32000, 512, 0, 0, False, False, True),      # lm_head fp32 logits
+    (577, 3072, 1024, 0, 0, True, False, False),      # ViT QKV
+    (1000, 4096, 1024, 0, 1, True, False, False),     # ViT FC1 QuickGELU
+    (1252, 2816, 512, 0, 4, False, False, False),     # prefill SwiGLU, normal mode
+    (4096, 1024, 4096, 2, 0, True, True, False),
+    (300, 512, 640, 0, 0, False, False, False),       # patch-embed K padding
+])
+def test_gemm(M, N, K, mode, act, bias, res, f32):
+    g = torch.Generator(device=DEV).manual_seed(M * 7 + N)
+    A = (torch.randn(M, K, device=DEV, generator=g) * 0.5).bfloat16()
+    W = (torch.randn(N, K, device=DEV, generator=g) * 0.05).bfloat16()
+    b = (torch.randn(N, device=DEV, generator=g) * 0.1).bfloat16() if bias else None
+    oc = N // 2 if act == _lib.HY_ACT_SWIGLU else N
+    r = torch.randn(M, oc, device=DEV, generator=g).bfloat16() if res else None
+    out = torch.empty(M, oc, device=DEV, dtype=torch.float32 if f32 else torch.bfloat16)
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device=DEV)
+    e = _lib.HyGemmEpilogue(_lib.ptr(b), _lib.ptr(r), oc, act, 0, out.data_ptr(), oc, int(f32))
+    ck(lib().hy_gemm_bf16_mode(A.data_ptr(), K, W.data_ptr(), K, M, N, K, e, ws.data_ptr(),
+                               ws.numel(), mode, st()), "gemm")
+    ref = _gemm_ref(A, W, b, act, r)
+    tol = 0.02 * max(1.0, ref.abs().max().item()) if not f32 else 2e-3 * max(1.0, ref.abs().max().item())
+    assert (out.float() - ref).abs().max().item() <= tol
+
+
+def test_gemm_row_map_and_inplace_residual():
+    M, N, K = 300, 512, 256
+    A = torch.randn(M, K, device=DEV).bfloat16()
+    W = (torch.randn(N, K, device=DEV) * 0.05).bfloat16()
+    x = torch.randn(M, N, device=DEV).bfloat16()
+    ref = A.float() @ W.float().T + x.float()
+    e = _lib.HyGemmEpilogue(0, x.data_ptr(), N, 0, 0, x.data_ptr(), N, 0)  # out aliases residual
+    ck(lib().hy_gemm_bf16(A.data_ptr(), K, W.data_ptr(), K, M, N, K, e, 0, 0, st()))
+    assert (x.float() - ref).abs().max().item() < 0.05
+    perm = torch.randperm(1000, device=DEV)[:M].to(torch.int32)
+    big = torch.zeros(1000, N, device=DEV, dtype=torch.bfloat16)
+    e = _lib.HyGemmEpilogue(0, 0, 0, 0, perm.data_ptr(), big.data_ptr(), N, 0)
+    ck(lib().hy_gemm_bf16(A.data_ptr(), K, W.data_ptr(), K, M, N, K, e, 0, 0, st()))
+    ref2 = (A.float() @ W.float().T)
+    assert (big[perm.long()].float() - ref2).abs().max().item() < 0.05
+
+
+# ---------------------------------------------------------------- norms
+def test_rmsnorm_layernorm_with_row_gather():
+    R, H = 37, 4096
+    x = torch.randn(100, H, device=DEV).bfloat16()
+    w = (1 + 0.1 * torch.randn(H, device=DEV)).bfloat16()
+    b = (0.1 * torch.randn(H, device=DEV)).bfloat16()
+    idx = torch.randint(0, 100, (R,), device=DEV, dtype=torch.int32)
+    out = torch.empty(R, H, device=DEV, dtype=torch.bfloat16)
+    ck(lib().hy_rmsnorm(x.data_ptr(), H, w.data_ptr(), out.data_ptr(), H, R, H, 1e-5,
+                        idx.data_ptr(), st()))
+    xs = x[idx.long()].float()
+    ref = xs / torch.sqrt((xs * xs).mean(-1, keepdim=True) + 1e-5) * w.float()
+    assert (out.float() - ref).abs().max().item() < 0.03
+    ck(lib().hy_layernorm(x.data_ptr(), H, w.data_ptr(), b.data_ptr(), out.data_ptr(), H, R, H,
+                          1e-5, idx.data_ptr(), st()))
+    ref = torch.nn.functional.layer_norm(xs, (H,), w.float(), b.float(), 1e-5)
+    assert (out.float() - ref).abs().max().item() < 0.03
+
+
+# ---------------------------------------------------------------- paged KV helpers
+def _paged_setup(n_seq, ctxs, n_kv, d, n_layers=2, layer=1, seed=0):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    nblk = [-(-c // 16) for c in ctxs]
+    total = sum(nblk) + 5
+    block_elems = n_layers * 2 * n_kv * 16 * d
+    kv = torch.randn(total, block_elems, device=DEV, generator=g).bfloat16()
+    perm = torch.randperm(total, generator=torch.Generator().manual_seed(seed)).tolist()
+    bt_stride = max(nblk) + 2
+    bt = torch.zeros(n_seq, bt_stride, dtype=torch.int32)
+    used = 0
+    for i, nb in enumerate(nblk):
+        bt[i, :nb] = torch.tensor(perm[used:used + nb], dtype=torch.int32)
+        used += nb
+    return kv, bt.to(DEV), bt_stride, block_elems
+
+
+def _gather_kv(kv, bt, i, ctx, n_layers, layer, n_kv, d):
+    lay = kv.view(kv.shape[0], n_layers, 2, n_kv, 16, d)[:, layer]
+    nb = -(-ctx // 16)
+    ids = bt[i, :nb].long()
+    K = lay[ids, 0].permute(0, 2, 1, 3).reshape(nb * 16, n_kv, d)[:ctx]
+    V = lay[ids, 1].permute(0, 2, 1, 3).reshape(nb * 16, n_kv, d)[:ctx]
+    return K.float(), V.float()
+
+
+@pytest.mark.parametrize("n_heads,n_kv,ctxs", [
+    (4, 4, [1, 17, 300, 33]),
+    (32, 32, [616, 617, 2000]),
+    (28, 4, [5, 900, 4097]),          # GQA group 7 (Qwen2-VL)
+    (8, 8, [16 * 64 * 3 + 5]),        # long context: split-KV combine path
+])
+def test_decode_attention(n_heads, n_kv, ctxs):
+    d, L, layer = 128, 2, 1
+    n = len(ctxs)
+    kv, bt, bts, be = _paged_setup(n, ctxs, n_kv, d, L, layer)
+    q = torch.randn(n, n_heads * d, device=DEV).bfloat16()
+    out = torch.empty(n, n_heads * d, device=DEV, dtype=torch.bfloat16)
+    slots = torch.arange(n, device=DEV, dtype=torch.int32)
+    ctx = torch.tensor(ctxs, device=DEV, dtype=torch.int32)
+    wsb = lib().hy_attn_decode_workspace_bytes(n, n_heads, d, max(ctxs))
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=DEV)
+    layer_ptr = kv.data_ptr() + layer * 2 * n_kv * 16 * d * 2
+    ck(lib().hy_attn_decode_paged(q.data_ptr(), n_heads * d, n, n_heads, n_kv, d,
+                                  slots.data_ptr(), ctx.data_ptr(), max(ctxs), bt.data_ptr(), bts,
+                                  layer_ptr, be, 1 / math.sqrt(d), out.data_ptr(), n_heads * d,
+                                  ws.data_ptr(), ws.numel(), st()), "decode")
+    grp = n_heads // n_kv
+    for i, c in enumerate(ctxs):
+        K, V = _gather_kv(kv, bt, i, c, L, layer, n_kv, d)
+        qi = q[i].float().view(n_heads, d)
+        Kx = K.repeat_interleave(grp, 1)
+        Vx = V.repeat_interleave(grp, 1)
+        s = torch.einsum("hd,thd->ht", qi, Kx) / math.sqrt(d)
+        ref = torch.einsum("ht,thd->hd", torch.softmax(s, -1), Vx).reshape(-1)
+        assert (out[i].float() - ref).abs().max().item() < 2e-2, (i, c)
+
+
+@pytest.mark.parametrize("n_heads,n_kv,chunks", [
+    (4, 4, [(0, 70), (100, 37), (16, 64)]),           # (offset, chunk)
+    (32, 32, [(0, 616)]),
+    (28, 4, [(576, 40), (0, 129)]),
+])
+def test_prefill_attention_paged(n_heads, n_kv, chunks):
+    d, L, layer = 128, 2, 0
+    ctxs = [o + c for o, c in chunks]
+    n = len(chunks)
+    kv, bt, bts, be = _paged_setup(n, ctxs, n_kv, d, L, layer, seed=1)
+    rows = sum(c for _, c in chunks)
+    q = torch.randn(rows, n_heads * d, device=DEV).bfloat16()
+    out = torch.empty(rows, n_heads * d, device=DEV, dtype=torch.bfloat16)
+    qstart = torch.tensor(np.cumsum([0] + [c for _, c in chunks]), dtype=torch.int32, device=DEV)
+    offs = torch.tensor([o for o, _ in chunks], dtype=torch.int32, device=DEV)
+    slots = torch.arange(n, dtype=torch.int32, device=DEV)
+    ck(lib().hy_attn_prefill_paged(q.data_ptr(), n_heads * d, n, qstart.data_ptr(),
+                                   offs.data_ptr(), slots.data_ptr(), max(c for _, c in chunks),
+                                   n_heads, n_kv, d, bt.data_ptr(), bts, kv.data_ptr(), be,
+                                   1 / math.sqrt(d), out.data_ptr(), n_heads * d, st()), "prefill")
+    grp = n_heads // n_kv
+    r0 = 0
+    for i, (o, c) in enumerate(chunks):
+        K, V = _gather_kv(kv, bt, i, o + c, L, layer, n_kv, d)
+        qi = q[r0:r0 + c].float().view(c, n_heads, d)
+        s = torch.einsum("qhd,thd->hqt", qi, K.repeat_interleave(grp, 1)) / math.sqrt(d)
+        mask = torch.arange(o + c, device=DEV)[None] > (o + torch.arange(c, device=DEV))[:, None]
+        s = s.masked_fill(mask[None], float("-inf"))
+        ref = torch.einsum("hqt,thd->qhd", torch.softmax(s, -1), V.repeat_interleave(grp, 1))
+        assert (out[r0:r0 + c].float() - ref.reshape(c, -1)).abs().max().item() < 2e-2, i
+        r0 += c
+
+
+@pytest.mark.parametrize("d,lens", [(64, [577, 577, 10]), (80, [1024, 64, 300]), (128, [65])])
+def test_vit_varlen_attention(d, lens):
+    nh = 4
+    T = sum(lens)
+    qkv = torch.randn(T, 3 * nh * d, device=DEV).bfloat16()
+    out = torch.empty(T, nh * d, device=DEV, dtype=torch.bfloat16)
+    seg = torch.tensor(np.cumsum([0] + lens), dtype=torch.int32, device=DEV)
+    ck(lib().hy_attn_varlen(qkv.data_ptr(), 3 * nh * d, len(lens), seg.data_ptr(), max(lens),
+                            nh, d, 1 / math.sqrt(d), out.data_ptr(), nh * d, st()), "varlen")
+    r0 = 0
+    for n in lens:
+        x = qkv[r0:r0 + n].float().view(n, 3, nh, d)
+        q, k, v = x[:, 0], x[:, 1], x[:, 2]
+        s = torch.einsum("qhd,khd->hqk", q, k) / math.sqrt(d)
+        ref = torch.einsum("hqk,khd->qhd", torch.softmax(s, -1), v).reshape(n, -1)
+        assert (out[r0:r0 + n].float() - ref).abs().max().item() < 2e-2
+        r0 += n
+
+
+def test_rope_kv_append():
+    nh, nkv, d, L, layer = 4, 2, 128, 3, 2
+    R = 40
+    pos = torch.tensor(list(range(0, 20)) + list(range(100, 120)), dtype=torch.int32, device=DEV)
+    slot = torch.tensor([0] * 20 + [1] * 20, dtype=torch.int32, device=DEV)
+    bt = torch.tensor([[5, 3, 0, 0, 0, 0, 0, 0], [1, 2, 4, 6, 0, 7, 8, 9]], dtype=torch.int32,
+                      device=DEV)
+    be = L * 2 * nkv * 16 * d
+    kv = torch.zeros(10, be, dtype=torch.bfloat16, device=DEV)
+    qkv = torch.randn(R, (nh + 2 * nkv) * d, device=DEV).bfloat16()
+    q0 = qkv.clone()
+    layer_ptr = kv.data_ptr() + layer * 2 * nkv * 16 * d * 2
+    ck(lib().hy_rope_kv_append(qkv.data_ptr(), qkv.shape[1], R, nh, nkv, d, pos.data_ptr(),
+                               slot.data_ptr(), bt.data_ptr(), 8, layer_ptr, be, 10000.0, st()))
+    inv = 1.0 / (10000.0 ** (torch.arange(0, d // 2, device=DEV).float() * 2 / d))
+    ang = pos.float()[:, None] * inv[None]
+    c, s = torch.cos(ang)[:, None], torch.sin(ang)[:, None]
+
+    def rope(x):
+        x1, x2 = x[..., :d // 2], x[..., d // 2:]
+        return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1)
+
+    x = q0.float().view(R, nh + 2 * nkv, d)
+    assert (qkv.float().view(R, -1, d)[:, :nh] - rope(x[:, :nh])).abs().max() < 2e-2
+    lay = kv.view(10, L, 2, nkv, 16, d)[:, layer]
+    for r in range(R):
+        p = int(pos[r]); b = int(bt[int(slot[r]), p // 16])
+        k_got = lay[b, 0, :, p % 16].float()
+        v_got = lay[b, 1, :, p % 16]
+        assert torch.equal(v_got, q0.view(R, -1, d)[r, nh + nkv:])
+        ang_r = p * inv
+        cr, sr = torch.cos(ang_r), torch.sin(ang_r)
+        kx = x[r, nh:nh + nkv]
+        kr = torch.cat([kx[:, :d // 2] * cr - kx[:, d // 2:] * sr,
+                        kx[:, d // 2:] * cr + kx[:, :d // 2] * sr], -1)
+        assert (k_got - kr).abs().max() < 2e-2
+
+
+# ---------------------------------------------------------------- byte/index kernels
+def test_argmax_first_maximum():
+    R, V = 5, 32000
+    x = torch.randn(R, V, device=DEV)
+    x[1, 7] = 100.0
+    x[1, 9] = 100.0      # tie -> first index
+    x[2, V - 1] = 50.0
+    out = torch.empty(R, dtype=torch.int32, device=DEV)
+    slot = torch.tensor([3, 0, 1, 2, 4], dtype=torch.int32, device=DEV)
+    last = torch.full((5,), -1, dtype=torch.int32, device=DEV)
+    ck(lib().hy_argmax_f32(x.data_ptr(), R, V, V, out.data_ptr(), slot.data_ptr(),
+                           last.data_ptr(), st()))
+    ref = x.argmax(-1).to(torch.int32)
+    assert torch.equal(out, ref)
+    assert out[1].item() == 7
+    assert torch.equal(last[slot.long()], ref)
+
+
+def test_copy_blocks_and_scatter_bit_exact():
+    nb, bb = 20, 8 << 10
+    src = torch.randint(0, 255, (nb, bb), dtype=torch.uint8, device=DEV)
+    dst = torch.zeros(nb, bb, dtype=torch.uint8, device=DEV)
+    s_ids = torch.tensor([3, 7, 0, 19], dtype=torch.int32, device=DEV)
+    d_ids = torch.tensor([0, 1, 5, 2], dtype=torch.int32, device=DEV)
+    ck(lib().hy_copy_blocks(src.data_ptr(), dst.data_ptr(), s_ids.data_ptr(), d_ids.data_ptr(),
+                            4, bb, st()))
+    for s, d in zip(s_ids.tolist(), d_ids.tolist()):
+        assert torch.equal(dst[d], src[s])
+    assert int(dst[3].sum()) == 0
+    t = torch.zeros(100, dtype=torch.int32, device=DEV)
+    idx = torch.tensor([5, 99, 0], dtype=torch.int32, device=DEV)
+    val = torch.tensor([1, 2, 3], dtype=torch.int32, device=DEV)
+    ck(lib().hy_scatter_i32(t.data_ptr(), idx.data_ptr(), val.data_ptr(), 3, st()))
+    assert t[5].item() == 1 and t[99].item() == 2 and t[0].item() == 3
+
+
+def test_merge_embed_bit_exact():
+    V, H = 50, 512
+    emb = torch.randn(V, H, device=DEV).bfloat16()
+    img = torch.randn(2 * 576, H, device=DEV).bfloat16()
+    last = torch.tensor([7, 9], dtype=torch.int32, device=DEV)
+    tok = torch.tensor([3, -1, -(1 + 600), _lib.HY_TOK_FROM_LAST, 49], dtype=torch.int32,
+                       device=DEV)
+    slot = torch.tensor([0, 0, 0, 1, 0], dtype=torch.int32, device=DEV)
+    out = torch.empty(5, H, device=DEV, dtype=torch.bfloat16)
+    ck(lib().hy_merge_embed(tok.data_ptr(), 5, emb.data_ptr(), img.data_ptr(), H, last.data_ptr(),
+                            slot.data_ptr(), out.data_ptr(), st()))
+    assert torch.equal(out[0], emb[3]) and torch.equal(out[1], img[0])
+    assert torch.equal(out[2], img[600]) and torch.equal(out[3], emb[9])
+    assert torch.equal(out[4], emb[49])
+
+
+@pytest.mark.parametrize("merge,gh,gw", [(1, 24, 24), (2, 4, 6)])
+def test_im2col_matches_oracle(merge, gh, gw):
+    from oracle.mllm_fp32 import OracleMLLM
+    p = 14
+    px = np.random.default_rng(0).integers(0, 256, (gh * p, gw * p, 3), dtype=np.uint8)
+    dpx = torch.from_numpy(px).to(DEV)
+    kp = 640
+    out = torch.empty(gh * gw, kp, dtype=torch.bfloat16, device=DEV)
+    desc = (_lib.HyImageDesc * 1)(_lib.HyImageDesc(dpx.data_ptr(), gw * p * 3, gh, gw, 0, 0, 0, 0))
+    dd = torch.frombuffer(bytearray(bytes(desc)), dtype=torch.uint8).to(DEV)
+    ck(lib().hy_im2col_patches(dd.data_ptr(), 1, gh * gw, p, merge, kp, out.data_ptr(), st()))
+    o = OracleMLLM.__new__(OracleMLLM)
+    o.s = {"patch": p, "merge": merge}
+    ref = o.im2col(px, gh, gw)
+    assert (out[:, :588].float().cpu() - ref).abs().max().item() < 2e-2
+    assert out[:, 588:].abs().max().item() == 0
