@@ -221,7 +221,7 @@ def run_ours(args, d: Dist):
     # ---- warm-up (untimed): short replays exercise every kernel shape class
     warm = E.Trace(base.requests[:24], name="warm")
     for i in range(args.warmup):
-        replay(50.0 * (i + 1), trace=warm)
+        replay(50.0 * (i + 1), trace=warm)[0].close()
     torch.cuda.synchronize()
 
     # ---- timed goodput search: K probes
@@ -256,6 +256,7 @@ def run_ours(args, d: Dist):
                            "device_busy_s": tot[4] / 1e3, "batches": int(tot[5]),
                            "ttft_p90": a["ttft_percentiles_s"].get("p90"),
                            "tbt_p90": a["tbt_percentiles_s"].get("p90")})
+        cl.close()
         return att
 
     best, probes = geometric_bisect(probe, args.rate_lo, args.rate_hi, args.steps)
@@ -314,10 +315,11 @@ def run_ours(args, d: Dist):
             tot = d.reduce([meets, len(rep.requests)])
             att = tot[0] / tot[1]
             e2e_probes.append((r * d.world, att))
+            n_img = sum(rt.stats["images"] for rt in cl.runtimes.values())
+            n_tok = sum(r_.tokens_out for r_ in cl.reqs.values())
+            cl.close()
             if att >= 0.9:
                 e2e_rate = r * d.world
-                n_img = sum(rt.stats["images"] for rt in cl.runtimes.values())
-                n_tok = sum(r_.tokens_out for r_ in cl.reqs.values())
                 break
         e2e = {"value": e2e_rate or 0.0, "unit": UNIT,
                "h2d_bytes_per_step": None, "d2h_bytes_per_step": None, "probes": e2e_probes,

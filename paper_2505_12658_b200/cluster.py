@@ -203,6 +203,16 @@ class GpuCluster(C.Cluster):
                 if not pool.consistent():
                     raise AssertionError(f"physical pool of {iid} disagrees with its counts")
 
+    def close(self) -> None:
+        """Drop every device buffer of this cluster (pools, tables, workspaces) so the
+        next cluster on the same GPU can reuse the memory; shared weights stay."""
+        for rt in self.runtimes.values():
+            rt.close()
+        self.runtimes = {}
+        self.jobs.clear()
+        import gc
+        gc.collect()
+
     def gpu_launch_count(self) -> int:
         return sum(rt.launches for rt in self.runtimes.values())
 

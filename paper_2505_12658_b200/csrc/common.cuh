@@ -140,6 +140,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Low-traffic wait for warps that idle for a whole main loop (epilogue): one lane
+// polls with exponential nanosleep backoff so the mbarrier unit stays free for the
+// TMA / MMA handshakes, then the warp reconverges.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleepy(uint64_t* bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t ns = 32;
+    while (!mbar_test(bar, parity)) {
+      __nanosleep(ns);
+      ns = ns < 512 ? ns * 2 : 512;
+    }
+  }
+  __syncwarp();
+  mbar_wait(bar, parity);  // completes immediately; gives every lane acquire semantics
+}
+
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* tm) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tm) : "memory");
 }

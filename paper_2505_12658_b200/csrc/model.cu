@@ -53,6 +53,9 @@ static size_t lang_carve(const HyLangModel* m, int max_rows, int max_out, int ma
   Carve c(base);
   const int qkv_cols = (m->n_heads + 2 * m->n_kv_heads) * m->head_dim;
   LangWs l{};
+  // the GEMM workspace holds stream-K arrival counters that must stay zero between
+  // calls: it lives at a fixed offset (the start), independent of the batch shape
+  l.gemm_ws = c.take<uint8_t>(kGemmWs);
   l.x = c.take<bf16>((size_t)max_rows * m->hidden);
   l.t = c.take<bf16>((size_t)max_rows * m->hidden);
   l.qkv = c.take<bf16>((size_t)max_rows * qkv_cols);
@@ -60,7 +63,6 @@ static size_t lang_carve(const HyLangModel* m, int max_rows, int max_out, int ma
   l.f = c.take<bf16>((size_t)max_rows * m->ffn);
   l.tout = c.take<bf16>((size_t)std::max(max_out, 1) * m->hidden);
   l.logits = c.take<float>((size_t)std::max(max_out, 1) * m->vocab);
-  l.gemm_ws = c.take<uint8_t>(kGemmWs);
   l.dec_ws_bytes =
       hy_attn_decode_workspace_bytes(std::max(max_decode, 1), m->n_heads, m->head_dim, max_ctx);
   l.dec_ws = c.take<uint8_t>(l.dec_ws_bytes);
@@ -168,6 +170,7 @@ struct VitWs {
 static size_t vit_carve(const HyVitModel* m, int max_tokens, void* base, VitWs* w) {
   Carve c(base);
   VitWs v{};
+  v.gemm_ws = c.take<uint8_t>(kGemmWs);  // fixed offset: see lang_carve
   const int Hv = m->hidden;
   v.patches = c.take<bf16>((size_t)max_tokens * m->k_pad);
   v.pe = c.take<bf16>((size_t)max_tokens * Hv);
@@ -178,7 +181,6 @@ static size_t vit_carve(const HyVitModel* m, int max_tokens, void* base, VitWs* 
   v.f = c.take<bf16>((size_t)max_tokens * std::max(m->mlp, m->proj_hidden));
   v.v = c.take<bf16>((size_t)max_tokens * Hv);
   v.p = c.take<bf16>((size_t)max_tokens * m->proj_hidden);
-  v.gemm_ws = c.take<uint8_t>(kGemmWs);
   if (w) *w = v;
   return c.off + 256;
 }

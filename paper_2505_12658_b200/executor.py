@@ -151,12 +151,12 @@ class InstanceRuntime:
             cap = self.lib.hy_lang_workspace_bytes(
                 self.weights.lang, max(rows, self.lang_max_rows), max(n_out, 1024),
                 max(n_dec, 1024), max(max_ctx, self.bt_stride * KVB))
-            self.lang_ws = torch.empty(max(need, cap), dtype=torch.uint8, device=self.device)
+            self.lang_ws = torch.zeros(max(need, cap), dtype=torch.uint8, device=self.device)
 
     def _ensure_vit_ws(self, tokens: int) -> None:
         need = self.lib.hy_vit_workspace_bytes(self.weights.vit, max(tokens, 1), 0)
         if self.vit_ws is None or self.vit_ws.numel() < need:
-            self.vit_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self.vit_ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
 
     def sync_block_tables(self, stream) -> None:
         """Push block lists of requests whose KV allocation changed to the device."""
@@ -468,6 +468,14 @@ class InstanceRuntime:
         _lib.check(lib.hy_vit_forward(self.weights.vit, vb, self.vit_ws.data_ptr(),
                                       self.vit_ws.numel(), sv.cuda_stream),
                    f"hy_vit_forward[{self.iid}]")
+
+    def close(self) -> None:
+        for name in ("kv", "img", "block_table", "last_tok", "lang_ws", "vit_ws", "tok_log",
+                     "meta", "vmeta", "pix", "_keep"):
+            if hasattr(self, name):
+                setattr(self, name, None)
+        self._img_dev.clear()
+        self.exec_log.clear()
 
     # ------------------------------------------------------------------ results
     def collect_tokens(self, out: Dict[str, List[int]]) -> None:

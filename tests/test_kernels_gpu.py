@@ -83,7 +83,7 @@ def test_gemm(M, N, K, mode, act, bias, res, f32):
     oc = N // 2 if act == _lib.HY_ACT_SWIGLU else N
     r = torch.randn(M, oc, device=DEV, generator=g).bfloat16() if res else None
     out = torch.empty(M, oc, device=DEV, dtype=torch.float32 if f32 else torch.bfloat16)
-    ws = torch.empty(64 << 20, dtype=torch.uint8, device=DEV)
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device=DEV)
     e = _lib.HyGemmEpilogue(_lib.ptr(b), _lib.ptr(r), oc, act, 0, out.data_ptr(), oc, int(f32))
     ck(lib().hy_gemm_bf16_mode(A.data_ptr(), K, W.data_ptr(), K, M, N, K, e, ws.data_ptr(),
                                ws.numel(), mode, st()), "gemm")
