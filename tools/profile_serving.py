@@ -1,0 +1,43 @@
+"""Short LLaVA-1.5-7B serving replay for ncu captures (profiles/).
+
+    python tools/profile_serving.py [--requests 48] [--rate 60]
+
+Runs the same path as bench.py (epdsim scheduler + GPU executor, device clock) on a short
+TextCaps-shaped trace, so `ncu --metrics gpu__time_duration.sum` gives the launch list
+of a real serving mix and `ncu --set full -k regex:<kernel>` captures representative
+launches.  Never a source of bench numbers (ncu serialises and replays kernels).
+"""
+
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--requests", type=int, default=48)
+    ap.add_argument("--rate", type=float, default=60.0)
+    ap.add_argument("--model", default="llava-1.5-7b")
+    args = ap.parse_args()
+    import torch
+    import paper_2505_12658_b200 as P
+    from paper_2505_12658_b200._epdsim import C, E
+    from paper_2505_12658_b200.cluster import GpuCluster
+    shape = P.get_shape(args.model)
+    slo = E.SloSpec(4.0, 0.08)
+    tr = E.synth_trace(seed=7, n_requests=args.requests, rate=args.rate, image_count_dist=1,
+                       visual_token_choices=576, prompt_dist=[25, 35, 45],
+                       output_dist=[90, 110, 130], slo=slo)
+    spec = C.ClusterSpec(method=C.DisaggregationMethod.parse("EPD:1"))
+    cl = GpuCluster(spec, shape, P.b200_hardware(), slo, clock="device")
+    rep = cl.run(tr)
+    torch.cuda.synchronize()
+    rt = next(iter(cl.runtimes.values()))
+    print("batches", rt.stats["batches"], "device_ms", round(rt.stats["device_ms"], 1),
+          "attainment", rep.aggregates["slo_attainment"])
+
+
+if __name__ == "__main__":
+    main()
