@@ -53,12 +53,17 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="llava-1.5-7b")
     ap.add_argument("--method", default="EPD:1")
-    ap.add_argument("--requests", type=int, default=600, help="trace requests per GPU")
-    ap.add_argument("--rate-lo", type=float, default=4.0, help="per-GPU req/s")
-    ap.add_argument("--rate-hi", type=float, default=160.0, help="per-GPU req/s")
+    # >= ~40 s of arrivals at the goodput rate, so a burst cannot drain inside the 4 s TTFT
+    # bound and pass a rate the GPU cannot sustain (finite-trace artifact)
+    ap.add_argument("--requests", type=int, default=1500, help="trace requests per GPU")
+    ap.add_argument("--rate-lo", type=float, default=16.0, help="per-GPU req/s")
+    ap.add_argument("--rate-hi", type=float, default=128.0, help="per-GPU req/s")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--budgets", default="measured", choices=["measured", "roofline"],
+                    help="per-batch token/image budgets: reference search over GPU-timed "
+                         "probes (SURVEY 8f f2) or over the reference roofline")
     return ap.parse_args()
 
 
@@ -206,12 +211,15 @@ def run_ours(args, d: Dist):
     base, slo = base_trace(E, args.requests * d.world)
     my = shard(E, base, d.rank, d.world)
     sampler = KernelSampler(dev, every=4)
+    budgets_seen = {}
 
     def replay(rate_total, clock="device", resident=True, sample=False, trace=None):
         tr = E.scale_to_rate(trace or base, rate_total)
         tr = shard(E, tr, d.rank, d.world) if trace is None else tr
         cl = GpuCluster(spec, shape, hw, slo, devices=[dev], clock=clock, seed=args.seed,
-                        resident_inputs=resident, weights=weights)
+                        resident_inputs=resident, weights=weights, budgets=args.budgets)
+        budgets_seen.update({t.name: [b.token_budget, b.image_budget]
+                             for t, b in cl.type_budgets.items()})
         if sample:
             for rt in cl.runtimes.values():
                 rt.sampler = sampler
@@ -350,7 +358,8 @@ def run_ours(args, d: Dist):
                        "rate_bounds_per_gpu": [args.rate_lo, args.rate_hi],
                        "parallelism": f"dp{d.world} (independent EPD replicas)",
                        "l2": "inputs larger than L2: 14 GB weights + paged KV streamed per step",
-                       "clock": "virtual clock advanced by CUDA-event time of each batch"},
+                       "clock": "virtual clock advanced by CUDA-event time of each batch",
+                       "budgets": {"mode": args.budgets, "tau_t_tau_e": budgets_seen}},
             "decode_tok_s": best_probe["decode_tok_s"] if best_probe else 0.0,
             "kv_migration_gbs": None,
             "probes": probe_info,

@@ -59,7 +59,8 @@ class GpuCluster(C.Cluster):
                  probe_image_tokens: int = MC.IMAGE_BLOCK_TOKENS, max_slots: int = 4096,
                  max_seq_tokens: int = 16384, record_batches: bool = False,
                  weights: Optional[Dict] = None, capture: bool = False,
-                 pool_bytes_limit: Optional[int] = None, profile_override=None):
+                 pool_bytes_limit: Optional[int] = None, profile_override=None,
+                 budgets: str = "roofline"):
         if clock not in CLOCKS:
             raise ValueError(f"clock must be one of {CLOCKS}")
         if not torch.cuda.is_available():
@@ -97,6 +98,13 @@ class GpuCluster(C.Cluster):
         self.migration_log: List = []
         self.transfer_stats = {"count": 0, "bytes": 0.0, "copied_bytes": 0, "seconds": 0.0}
         self.generated: Dict[str, List[int]] = {}
+        # per-batch budgets: the reference's roofline search (decisions identical to the
+        # reference) or the same search over GPU-timed probe batches
+        if budgets == "measured":
+            from .budgets import measured_budgets
+            measured_budgets(self)
+        elif budgets != "roofline":
+            raise ValueError("budgets must be 'roofline' or 'measured'")
 
     # ------------------------------------------------------------------ S1
     def _try_schedule(self, iid: str) -> None:

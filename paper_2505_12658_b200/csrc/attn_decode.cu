@@ -29,6 +29,8 @@ __global__ void __launch_bounds__(128)
                        int bt_stride, const bf16* __restrict__ kv, long long block_stride,
                        float scale_log2, int blocks_per_split, bf16* __restrict__ out, int ld_o,
                        float* __restrict__ part, int nsplit) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int D = 128;
   const int b = blockIdx.x, kh = blockIdx.y, sp = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -158,6 +160,8 @@ __global__ void __launch_bounds__(128)
 
 __global__ void attn_decode_combine_kernel(const float* __restrict__ part, int n_heads, int nsplit,
                                            bf16* __restrict__ out, int ld_o) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int D = 128;
   const int b = blockIdx.x, h = blockIdx.y, d = threadIdx.x;
   const float* pp = part + ((size_t)b * n_heads + h) * nsplit * (D + 2);
@@ -214,9 +218,9 @@ extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads,
   float* part = reinterpret_cast<float*>(workspace);
 #define HY_DEC_CASE(GG)                                                                        \
   case GG:                                                                                     \
-    attn_decode_kernel<GG><<<grid, 128, 0, stream>>>(qp, ld_q, n_kv_heads, slots, ctx,         \
+    HY_CUDA_RET(launch_pdl(attn_decode_kernel<GG>, dim3(grid), dim3(128), 0, stream, qp, ld_q, n_kv_heads, slots, ctx,         \
                                                      block_table, bt_stride, kvp, block_stride, \
-                                                     sl2, bps, op, ld_o, part, ns);            \
+                                                     sl2, bps, op, ld_o, part, ns));            \
     break;
   switch (G) {
     HY_DEC_CASE(1)
@@ -231,7 +235,7 @@ extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads,
 #undef HY_DEC_CASE
   HY_LAUNCH_CHECK();
   if (ns > 1) {
-    attn_decode_combine_kernel<<<dim3(n, n_heads), 128, 0, stream>>>(part, n_heads, ns, op, ld_o);
+    HY_CUDA_RET(launch_pdl(attn_decode_combine_kernel, dim3(dim3(n, n_heads)), dim3(128), 0, stream, part, n_heads, ns, op, ld_o));
     HY_LAUNCH_CHECK();
   }
   return 0;

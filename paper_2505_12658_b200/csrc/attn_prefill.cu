@@ -72,6 +72,8 @@ __device__ __forceinline__ void mma_bf16_16816(float* c, uint32_t a0, uint32_t a
 
 template <int D, bool PAGED>
 __global__ void __launch_bounds__(128) attn_fa2_kernel(const FaParams p) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int BQ = 64, BKV = 64, LDS = D + 8;  // padded smem rows: conflict-free ldmatrix
   constexpr int CPR = D / 8;                     // 16-byte chunks per row
   extern __shared__ __align__(128) uint8_t fa_smem[];
@@ -257,7 +259,7 @@ static int launch_fa(const FaParams& p, int n_seqs, int n_heads, cudaStream_t st
     attr = true;
   }
   dim3 grid(n_seqs * p.q_tiles, n_heads);
-  attn_fa2_kernel<D, PAGED><<<grid, 128, smem, st>>>(p);
+  HY_CUDA_RET(launch_pdl(attn_fa2_kernel<D, PAGED>, dim3(grid), dim3(128), smem, st, p));
   HY_LAUNCH_CHECK();
   return 0;
 }

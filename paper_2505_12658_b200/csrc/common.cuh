@@ -10,6 +10,7 @@
 
 #include <cstdio>
 #include <string>
+#include <utility>
 
 namespace hy {
 
@@ -273,5 +274,35 @@ int num_sms();
 
 // kernel-class timer hooks (see hy_set_kernel_timer)
 void timer_mark(int klass, cudaStream_t st, bool begin, double work);
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch.  Every kernel of the serving path is launched with
+// programmatic stream serialisation: it lets its dependent grid launch as soon as all of
+// its own CTAs are resident (pdl_trigger at entry) and touches data written by earlier
+// kernels only after pdl_wait.  Work that reads nothing produced on the stream (the
+// GEMM's weight tiles, barrier init, TMEM allocation) overlaps the previous kernel.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace hy

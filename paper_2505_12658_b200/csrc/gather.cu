@@ -20,6 +20,8 @@ __global__ void merge_embed_kernel(const int* __restrict__ tok, int rows, const 
                                    const bf16* __restrict__ image_rows, int hidden,
                                    const int* __restrict__ last_tok, const int* __restrict__ row_slot,
                                    bf16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   int r = blockIdx.x;
   if (r >= rows) return;
   int t = tok[r];
@@ -44,6 +46,8 @@ __global__ void rope_kv_append_kernel(bf16* __restrict__ qkv, int ld_qkv, int ro
                                       const int* __restrict__ row_slot,
                                       const int* __restrict__ block_table, int bt_stride,
                                       bf16* __restrict__ kv, long long block_stride, float theta) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   if (r >= rows) return;
   const int p = pos[r];
@@ -100,6 +104,8 @@ __global__ void rope_kv_append_kernel(bf16* __restrict__ qkv, int ld_qkv, int ro
 __global__ void argmax_kernel(const float* __restrict__ logits, int rows, int vocab, int ld,
                               int* __restrict__ out_idx, const int* __restrict__ out_slot,
                               int* __restrict__ last_tok) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   if (r >= rows) return;
   const float* x = logits + (size_t)r * ld;
@@ -178,6 +184,8 @@ __device__ __forceinline__ void patch_coords(int i, int gw, int merge, int& py, 
 
 __global__ void im2col_kernel(const HyImageDesc* __restrict__ images, int n_images, int n_patches,
                               int patch, int merge, int k_pad, bf16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int pr = blockIdx.x;
   if (pr >= n_patches) return;
   const int ii = find_image(images, n_images, pr, 1);
@@ -210,6 +218,8 @@ __global__ void vit_assemble_kernel(const HyImageDesc* __restrict__ images, int 
                                     const bf16* __restrict__ pos_emb, int max_pos,
                                     const bf16* __restrict__ ln_w, const bf16* __restrict__ ln_b,
                                     float eps, bf16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int warps = blockDim.x >> 5;
   const int t = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -256,6 +266,8 @@ __global__ void vit_assemble_kernel(const HyImageDesc* __restrict__ images, int 
 __global__ void vit_gather_visual_kernel(const HyImageDesc* __restrict__ images, int n_images,
                                          int n_visual, int hidden, int cls,
                                          const bf16* __restrict__ h, bf16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int v = blockIdx.x;
   if (v >= n_visual) return;
   const int ii = find_image(images, n_images, v, 2);
@@ -272,6 +284,8 @@ __global__ void vit_gather_visual_kernel(const HyImageDesc* __restrict__ images,
 __global__ void copy_blocks_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                                    const int* __restrict__ src_ids, const int* __restrict__ dst_ids,
                                    long long block_bytes) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.y;
   const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)src_ids[b] * block_bytes);
   uint4* d = reinterpret_cast<uint4*>(dst + (size_t)dst_ids[b] * block_bytes);
@@ -304,6 +318,8 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 __global__ void fill_uniform_kernel(bf16* __restrict__ dst, long long rows, long long cols,
                                     long long ld, uint64_t key, float scale, float offset,
                                     int perm) {
+  pdl_trigger();
+  pdl_wait();
   const long long total = rows * ld;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
@@ -333,9 +349,9 @@ extern "C" int hy_merge_embed(const int* tok, int rows, const void* embed, const
                               cudaStream_t stream) {
   HY_CHECK_ARG(hidden % 8 == 0, "hidden % 8");
   if (rows <= 0) return 0;
-  merge_embed_kernel<<<rows, 128, 0, stream>>>(tok, rows, reinterpret_cast<const bf16*>(embed),
+  HY_CUDA_RET(launch_pdl(merge_embed_kernel, dim3(rows), dim3(128), 0, stream, tok, rows, reinterpret_cast<const bf16*>(embed),
                                                reinterpret_cast<const bf16*>(image_rows), hidden,
-                                               last_tok, row_slot, reinterpret_cast<bf16*>(out));
+                                               last_tok, row_slot, reinterpret_cast<bf16*>(out)));
   HY_LAUNCH_CHECK();
   return 0;
 }
@@ -346,9 +362,9 @@ extern "C" int hy_rope_kv_append(void* qkv, int ld_qkv, int rows, int n_heads, i
                                  long long block_stride, float rope_theta, cudaStream_t stream) {
   HY_CHECK_ARG(head_dim % 4 == 0 && ld_qkv % 2 == 0, "rope: head_dim % 4");
   if (rows <= 0) return 0;
-  rope_kv_append_kernel<<<rows, 256, 0, stream>>>(
+  HY_CUDA_RET(launch_pdl(rope_kv_append_kernel, dim3(rows), dim3(256), 0, stream, 
       reinterpret_cast<bf16*>(qkv), ld_qkv, rows, n_heads, n_kv_heads, head_dim, pos, row_slot,
-      block_table, bt_stride, reinterpret_cast<bf16*>(kv_layer), block_stride, rope_theta);
+      block_table, bt_stride, reinterpret_cast<bf16*>(kv_layer), block_stride, rope_theta));
   HY_LAUNCH_CHECK();
   return 0;
 }
@@ -356,7 +372,7 @@ extern "C" int hy_rope_kv_append(void* qkv, int ld_qkv, int rows, int n_heads, i
 extern "C" int hy_argmax_f32(const float* logits, int rows, int vocab, int ld, int* out_idx,
                              const int* out_slot, int* last_tok, cudaStream_t stream) {
   if (rows <= 0) return 0;
-  argmax_kernel<<<rows, 256, 0, stream>>>(logits, rows, vocab, ld, out_idx, out_slot, last_tok);
+  HY_CUDA_RET(launch_pdl(argmax_kernel, dim3(rows), dim3(256), 0, stream, logits, rows, vocab, ld, out_idx, out_slot, last_tok));
   HY_LAUNCH_CHECK();
   return 0;
 }
@@ -365,8 +381,8 @@ extern "C" int hy_im2col_patches(const HyImageDesc* images, int n_images, int n_
                                  int merge, int k_pad, void* patches, cudaStream_t stream) {
   HY_CHECK_ARG(k_pad >= 3 * patch * patch, "k_pad");
   if (n_patches <= 0) return 0;
-  im2col_kernel<<<n_patches, 128, 0, stream>>>(images, n_images, n_patches, patch, merge, k_pad,
-                                               reinterpret_cast<bf16*>(patches));
+  HY_CUDA_RET(launch_pdl(im2col_kernel, dim3(n_patches), dim3(128), 0, stream, images, n_images, n_patches, patch, merge, k_pad,
+                                               reinterpret_cast<bf16*>(patches)));
   HY_LAUNCH_CHECK();
   return 0;
 }
@@ -381,9 +397,9 @@ extern "C" int hy_copy_blocks(const void* src_base, void* dst_base, const int* s
   long long want = (n16 + threads * 4 - 1) / (threads * 4);
   int gx = (int)(want < 256 ? (want < 1 ? 1 : want) : 256);
   dim3 grid(gx, n);
-  copy_blocks_kernel<<<grid, threads, 0, stream>>>(reinterpret_cast<const uint8_t*>(src_base),
+  HY_CUDA_RET(launch_pdl(copy_blocks_kernel, dim3(grid), dim3(threads), 0, stream, reinterpret_cast<const uint8_t*>(src_base),
                                                    reinterpret_cast<uint8_t*>(dst_base), src_ids,
-                                                   dst_ids, block_bytes);
+                                                   dst_ids, block_bytes));
   HY_LAUNCH_CHECK();
   return 0;
 }
@@ -399,8 +415,8 @@ extern "C" int hy_fill_uniform_bf16(void* dst, long long rows, long long cols, l
   int threads = 256;
   long long blocks = (total + threads - 1) / threads;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  fill_uniform_kernel<<<(unsigned)blocks, threads, 0, stream>>>(
-      reinterpret_cast<bf16*>(dst), rows, cols, ld, key, scale, offset, perm);
+  HY_CUDA_RET(launch_pdl(fill_uniform_kernel, dim3((unsigned)blocks), dim3(threads), 0, stream, 
+      reinterpret_cast<bf16*>(dst), rows, cols, ld, key, scale, offset, perm));
   HY_LAUNCH_CHECK();
   return 0;
 }
@@ -408,6 +424,8 @@ extern "C" int hy_fill_uniform_bf16(void* dst, long long rows, long long cols, l
 // device metadata maintenance: dst[idx[i]] = val[i] (block-table rows)
 __global__ void scatter_i32_kernel(int* __restrict__ dst, const int* __restrict__ idx,
                                    const int* __restrict__ val, int n) {
+  pdl_trigger();
+  pdl_wait();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[idx[i]] = val[i];
 }
@@ -415,7 +433,7 @@ __global__ void scatter_i32_kernel(int* __restrict__ dst, const int* __restrict_
 extern "C" int hy_scatter_i32(int* dst, const int* idx, const int* val, int n,
                               cudaStream_t stream) {
   if (n <= 0) return 0;
-  scatter_i32_kernel<<<(n + 255) / 256, 256, 0, stream>>>(dst, idx, val, n);
+  HY_CUDA_RET(launch_pdl(scatter_i32_kernel, dim3((n + 255) / 256), dim3(256), 0, stream, dst, idx, val, n));
   HY_LAUNCH_CHECK();
   return 0;
 }
@@ -449,20 +467,20 @@ int vit_assemble(const HyImageDesc* images, int n_images, int n_tokens, int hidd
   if (n_tokens <= 0) return 0;
   HY_CHECK_ARG(hidden % 8 == 0, "vit hidden % 8");
   const int threads = 256;
-  vit_assemble_kernel<<<ceil_div(n_tokens, threads / 32), threads, 0, st>>>(
+  HY_CUDA_RET(launch_pdl(vit_assemble_kernel, dim3(ceil_div(n_tokens, threads / 32)), dim3(threads), 0, st, 
       images, n_images, n_tokens, hidden, cls, reinterpret_cast<const bf16*>(patch_rows),
       reinterpret_cast<const bf16*>(cls_emb), reinterpret_cast<const bf16*>(pos_emb), max_pos,
       reinterpret_cast<const bf16*>(ln_w), reinterpret_cast<const bf16*>(ln_b), eps,
-      reinterpret_cast<bf16*>(out));
+      reinterpret_cast<bf16*>(out)));
   HY_LAUNCH_CHECK();
   return 0;
 }
 int vit_gather_visual(const HyImageDesc* images, int n_images, int n_visual, int hidden, int cls,
                       const void* h, void* out, cudaStream_t st) {
   if (n_visual <= 0) return 0;
-  vit_gather_visual_kernel<<<n_visual, 128, 0, st>>>(images, n_images, n_visual, hidden, cls,
+  HY_CUDA_RET(launch_pdl(vit_gather_visual_kernel, dim3(n_visual), dim3(128), 0, st, images, n_images, n_visual, hidden, cls,
                                                      reinterpret_cast<const bf16*>(h),
-                                                     reinterpret_cast<bf16*>(out));
+                                                     reinterpret_cast<bf16*>(out)));
   HY_LAUNCH_CHECK();
   return 0;
 }

@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(192, 1)
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x;
   const int cta = blockIdx.x;
+  pdl_trigger();  // all CTAs are resident from the start (persistent grid <= #SMs)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -255,19 +256,51 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      int stage = 0;
-      uint32_t phase = 0;
       const uint64_t hintA = SWAP ? kEvictFirst : kEvictNormal;  // decode weights stream once
       const uint64_t hintB = SWAP ? kEvictLast : kEvictNormal;
+      // weight tile = A in swap orientation, B otherwise; activations are the other one
+      auto load_w = [&](int st, int kb, int p, int q) {
+        if (SWAP)
+          tma_load_2d(&tmA, &full[st], sA + st * C::A_BYTES, kb * C::BK, p * C::BM, hintA);
+        else
+          tma_load_2d(&tmB, &full[st], sB + st * C::B_BYTES, kb * C::BK, q * BN, hintB);
+      };
+      auto load_x = [&](int st, int kb, int p, int q) {
+        if (SWAP)
+          tma_load_2d(&tmB, &full[st], sB + st * C::B_BYTES, kb * C::BK, q * BN, hintB);
+        else
+          tma_load_2d(&tmA, &full[st], sA + st * C::A_BYTES, kb * C::BK, p * C::BM, hintA);
+      };
+      // (1) before the grid dependency resolves: weight tiles of the first stages (the
+      //     weights are never written on the stream, so this overlaps the previous kernel)
+      int npre = 0;
+      for (int i = 0; i < nseg && npre < C::STAGES; ++i) {
+        const Seg sg = get_segment(a, cta, G, i, su0, su1);
+        int p, q;
+        raster_tile(sg.tile, a, p, q);
+        for (int kb = sg.kb0; kb < sg.kb1 && npre < C::STAGES; ++kb, ++npre) {
+          mbar_expect_tx(&full[npre], C::STAGE_BYTES);
+          load_w(npre, kb, p, q);
+        }
+      }
+      pdl_wait();
+      // (2) everything in order; prefetched stages only need their activation tile
+      int stage = 0;
+      uint32_t phase = 0;
+      int g = 0;
       for (int i = 0; i < nseg; ++i) {
         const Seg sg = get_segment(a, cta, G, i, su0, su1);
         int p, q;
         raster_tile(sg.tile, a, p, q);
-        for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(&tmA, &full[stage], sA + stage * C::A_BYTES, kb * C::BK, p * C::BM, hintA);
-          tma_load_2d(&tmB, &full[stage], sB + stage * C::B_BYTES, kb * C::BK, q * BN, hintB);
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++g) {
+          if (g < npre) {
+            load_x(stage, kb, p, q);
+          } else {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+            load_w(stage, kb, p, q);
+            load_x(stage, kb, p, q);
+          }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -312,6 +345,7 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ---------------- epilogue warps 2..5 ----------------
+    pdl_wait();  // residuals, partials and counters are written by earlier kernels
     const int sub = warp & 3;  // TMEM lane sub-partition this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -426,7 +460,7 @@ static int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const GemmA
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
     attr_set = true;
   }
-  gemm_tc_kernel<BN, SWAP, EPI><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tA, tB, a);
+  HY_CUDA_RET(launch_pdl(gemm_tc_kernel<BN, SWAP, EPI>, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES, st, tA, tB, a));
   HY_LAUNCH_CHECK();
   return 0;
 }

@@ -10,6 +10,8 @@ template <bool LAYER>
 __global__ void norm_kernel(const bf16* __restrict__ x, int ldx, const bf16* __restrict__ w,
                             const bf16* __restrict__ b, bf16* __restrict__ out, int ldo, int rows,
                             int cols, float eps, const int* __restrict__ row_idx) {
+  pdl_trigger();
+  pdl_wait();
   const int warps = blockDim.x >> 5;
   const int r = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -61,10 +63,10 @@ static int launch_norm(const void* x, int ldx, const void* w, const void* b, voi
   if (rows <= 0) return 0;
   const int threads = 256;
   const int rows_per_block = threads / 32;
-  norm_kernel<LAYER><<<ceil_div(rows, rows_per_block), threads, 0, st>>>(
+  HY_CUDA_RET(launch_pdl(norm_kernel<LAYER>, dim3(ceil_div(rows, rows_per_block)), dim3(threads), 0, st, 
       reinterpret_cast<const bf16*>(x), ldx, reinterpret_cast<const bf16*>(w),
       reinterpret_cast<const bf16*>(b), reinterpret_cast<bf16*>(out), ldo, rows, cols, eps,
-      row_idx);
+      row_idx));
   HY_LAUNCH_CHECK();
   return 0;
 }
