@@ -36,6 +36,22 @@
 
 namespace hy {
 
+#ifdef HY_TRACE
+// Debug timeline (lab builds only): %globaltimer stamps of CTA 0 at fixed points.
+__device__ unsigned long long g_trace[32];
+__device__ __forceinline__ void trace(int i) {
+  if (blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_trace[i] = t;
+    g_trace[16 + i] = clock64();
+  }
+}
+#define HY_TR(i) trace(i)
+#else
+#define HY_TR(i)
+#endif
+
 enum EpiKind : int { EPI_BF16 = 0, EPI_QGELU = 1, EPI_GELU = 2, EPI_SWIGLU = 4, EPI_F32 = 5 };
 
 struct GemmArgs {
@@ -51,7 +67,7 @@ struct GemmArgs {
   void* out;
   int ldc;
   float* partial;  // [G][2][128][BN] fp32: first / last stream-K segment of each CTA
-  int* counters;   // [2G][4] arrival counters per stream-K tile and epilogue warp (zeroed)
+  int* counters;   // [tiles][8] arrival counters per stream-K tile and epilogue warp (zeroed)
 };
 
 template <int EPI>
@@ -61,85 +77,131 @@ __device__ __forceinline__ float act_of(float x) {
   return x;
 }
 
-// Normal orientation: this thread owns token row m and physical columns n0..n0+31.
-template <int EPI>
-__device__ __forceinline__ void epi_rows(const GemmArgs& a, int m, int n0, float* v) {
-  if (m >= a.M || n0 >= a.N) return;
-  if (a.bias) {
-#pragma unroll
-    for (int j = 0; j < 32; j += 8) {
-      float b[8];
-      load_bf16x8(a.bias + n0 + j, b);
-#pragma unroll
-      for (int t = 0; t < 8; ++t) v[j + t] += b[t];
-    }
-  }
-  constexpr int CNT = EPI == EPI_SWIGLU ? 16 : 32;
-  const int col0 = EPI == EPI_SWIGLU ? n0 / 2 : n0;
-  if (EPI == EPI_SWIGLU) {
-    // physical cols [32g, 32g+16) gate, [32g+16, 32g+32) up -> outputs [16g, 16g+16)
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = v[j] / (1.0f + __expf(-v[j])) * v[16 + j];
-  } else if (EPI == EPI_QGELU || EPI == EPI_GELU) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = act_of<EPI>(v[j]);
-  }
-  if (a.residual) {
-    const bf16* r = a.residual + (size_t)m * a.ldr + col0;
-#pragma unroll
-    for (int j = 0; j < CNT; j += 8) {
-      float b[8];
-      load_bf16x8(r + j, b);
-#pragma unroll
-      for (int t = 0; t < 8; ++t) v[j + t] += b[t];
-    }
-  }
-  const size_t row = a.row_map ? (size_t)a.row_map[m] : (size_t)m;
-  if (EPI == EPI_F32) {
-    float* o = reinterpret_cast<float*>(a.out) + row * a.ldc + col0;
-#pragma unroll
-    for (int j = 0; j < CNT; j += 4)
-      *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-  } else {
-    bf16* o = reinterpret_cast<bf16*>(a.out) + row * a.ldc + col0;
-#pragma unroll
-    for (int j = 0; j < CNT; j += 8) store_bf16x8(o + j, v + j);
-  }
-}
+// Epilogue of one 32 x 32 accumulator chunk of one epilogue warp.
+//
+// The TMEM load gives each lane one accumulator row (normal: a token row, 32 weight
+// columns; swap: a weight row, 32 tokens).  Bias and activation are applied in registers.
+// Normal orientation: each lane stores its row's outputs directly (16-byte vectors).
+// Swap orientation: a lane holds one output COLUMN, so the chunk is staged in shared
+// memory as fp32 [32 token rows][OC cols] and written back row-contiguous (8 outputs =
+// one 16-byte vector per lane) instead of 32 scattered 2-byte stores per lane; the
+// residual is read with the same coalesced pattern and added in fp32 before the single
+// rounding to bf16.
+constexpr int kEpiWarps = 8;             // two per TMEM lane sub-partition (even / odd chunks)
+constexpr int kStgStride = 32 * 4 + 16;  // bytes per staged row (pad: conflict-free 16B access)
+constexpr int kStgBytes = 16 * kStgStride;  // per epilogue warp: 16 token rows per pass
 
-// Swap orientation: this thread owns weight row n and tokens m0..m0+31 (warp-coalesced
-// along n).  SwiGLU pairs rows n and n+16 of the same warp through a shuffle.
-template <int EPI>
-__device__ __forceinline__ void epi_cols(const GemmArgs& a, int n, int m0, float* v, int lane) {
-  const bool nok = n < a.N;
-  const float b = (a.bias && nok) ? __bfloat162float(a.bias[n]) : 0.f;
-  int col = n;
-  bool writer = nok;
-  if (EPI == EPI_SWIGLU) {
+template <int EPI, bool SWAP>
+__device__ __forceinline__ void epi_chunk(const GemmArgs& a, int p0, int q0, float* v, int lane,
+                                          uint32_t stg) {
+  constexpr int OC = EPI == EPI_SWIGLU ? 16 : 32;  // output columns of this chunk
+  int row0, col0;  // first output row (token), first output column
+  if (!SWAP) {
+    // lane = token row p0 + lane; registers = weight columns q0..q0+31
+    if (q0 >= a.N) return;
+    if (a.bias) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float x = v[j] + b;
-      const float up = __shfl_down_sync(0xffffffffu, x, 16);
-      v[j] = x / (1.0f + __expf(-x)) * up;
+      for (int j = 0; j < 32; j += 8) {
+        float b[8];
+        load_bf16x8(a.bias + q0 + j, b);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[j + t] += b[t];
+      }
     }
-    writer = nok && lane < 16;
-    col = (n >> 5) * 16 + (n & 15);
-  } else {
+    if (EPI == EPI_SWIGLU) {
+      // physical cols [32g, 32g+16) gate, [32g+16, 32g+32) up -> outputs [16g, 16g+16)
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = act_of<EPI>(v[j] + b);
+      for (int j = 0; j < 16; ++j) v[j] = v[j] / (1.0f + __expf(-v[j])) * v[16 + j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = act_of<EPI>(v[j]);
+    }
+    // direct row stores: each lane already owns OC contiguous outputs of one row (measured
+    // faster than staging for this orientation: the chunk latency is the limiter, not sectors)
+    const int m = p0 + lane;
+    col0 = EPI == EPI_SWIGLU ? q0 / 2 : q0;
+    if (m < a.M) {
+      if (a.residual) {
+        const bf16* r = a.residual + (size_t)m * a.ldr + col0;
+#pragma unroll
+        for (int j = 0; j < OC; j += 8) {
+          float b[8];
+          load_bf16x8(r + j, b);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) v[j + t] += b[t];
+        }
+      }
+      const size_t row = a.row_map ? (size_t)a.row_map[m] : (size_t)m;
+      if (EPI == EPI_F32) {
+        float* o = reinterpret_cast<float*>(a.out) + row * a.ldc + col0;
+#pragma unroll
+        for (int j = 0; j < OC; j += 4)
+          *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+        bf16* o = reinterpret_cast<bf16*>(a.out) + row * a.ldc + col0;
+#pragma unroll
+        for (int j = 0; j < OC; j += 8) store_bf16x8(o + j, v + j);
+      }
+    }
+    return;
+  } else {
+    // lane = weight row p0 + lane; registers = tokens q0..q0+31
+    if (p0 >= a.N) return;
+    const int n = p0 + lane;
+    const float b = a.bias ? __bfloat162float(a.bias[n]) : 0.f;
+    if (EPI == EPI_SWIGLU) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float x = v[j] + b;
+        const float up = __shfl_down_sync(0xffffffffu, x, 16);
+        v[j] = x / (1.0f + __expf(-x)) * up;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = act_of<EPI>(v[j] + b);
+    }
+    row0 = q0;
+    col0 = EPI == EPI_SWIGLU ? p0 / 2 : p0;
   }
-  if (!writer) return;
-#pragma unroll 4
-  for (int j = 0; j < 32; ++j) {
-    const int m = m0 + j;
-    if (m >= a.M) break;
-    float x = v[j];
-    if (a.residual) x += __bfloat162float(a.residual[(size_t)m * a.ldr + col]);
-    const size_t row = a.row_map ? (size_t)a.row_map[m] : (size_t)m;
-    if (EPI == EPI_F32)
-      reinterpret_cast<float*>(a.out)[row * a.ldc + col] = x;
-    else
-      reinterpret_cast<bf16*>(a.out)[row * a.ldc + col] = __float2bfloat16_rn(x);
+  // two passes of 16 token rows through the staging buffer; L lanes per row, 8 outputs
+  // per lane, 32 / L rows per warp store
+  constexpr int L = OC / 8;
+  constexpr int RPI = 32 / L;
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    if (lane < OC) {
+      const uint32_t d = stg + lane * 4;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) sts_f32(d + j * kStgStride, v[pass * 16 + j]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < (16 + RPI - 1) / RPI; ++it) {
+      const int r = it * RPI + lane / L;
+      const int k = (lane % L) * 8;
+      const int m = row0 + pass * 16 + r;
+      if (r < 16 && m < a.M) {
+        const uint32_t s4 = stg + r * kStgStride + k * 4;
+        const float4 x0 = lds_f32x4(s4), x1 = lds_f32x4(s4 + 16);
+        float o[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        if (a.residual) {
+          float rr[8];
+          load_bf16x8(a.residual + (size_t)m * a.ldr + col0 + k, rr);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) o[t] += rr[t];
+        }
+        const size_t row = a.row_map ? (size_t)a.row_map[m] : (size_t)m;
+        if (EPI == EPI_F32) {
+          float4* dst =
+              reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + row * a.ldc + col0 + k);
+          dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+          dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+        } else {
+          store_bf16x8(reinterpret_cast<bf16*>(a.out) + row * a.ldc + col0 + k, o);
+        }
+      }
+    }
+    __syncwarp();  // staging buffer is reused by the next pass / chunk
   }
 }
 
@@ -153,8 +215,9 @@ struct GemmCfg {
   static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int THREADS = 192;
+  static constexpr int SMEM_BYTES =
+      STAGES * STAGE_BYTES + kEpiWarps * kStgBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int THREADS = 64 + 32 * kEpiWarps;
 };
 
 // raster index -> (p, q): groups of 8 p-tiles sweep all q-tiles (L2 reuse)
@@ -209,7 +272,7 @@ __device__ __forceinline__ Seg get_segment(const GemmArgs& a, int c, int G, int 
 }
 
 template <int BN, bool SWAP, int EPI>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs a) {
   using C = GemmCfg<BN>;
@@ -218,7 +281,8 @@ __global__ void __launch_bounds__(192, 1)
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* stg_base = smem + C::STAGES * C::STAGE_BYTES;  // 4 epilogue staging buffers
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + kEpiWarps * kStgBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
@@ -229,6 +293,7 @@ __global__ void __launch_bounds__(192, 1)
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x;
   const int cta = blockIdx.x;
+  if (threadIdx.x == 0) HY_TR(0);
   pdl_trigger();  // all CTAs are resident from the start (persistent grid <= #SMs)
 
   if (warp == 0 && lane == 0) {
@@ -240,7 +305,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], kEpiWarps);
     }
     fence_mbar_init();
   }
@@ -249,6 +314,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) HY_TR(1);
 
   long long su0, su1;
   const int nseg = cta_segments(a, cta, G, su0, su1);
@@ -283,7 +349,9 @@ __global__ void __launch_bounds__(192, 1)
           load_w(npre, kb, p, q);
         }
       }
+      HY_TR(2);
       pdl_wait();
+      HY_TR(3);
       // (2) everything in order; prefetched stages only need their activation tile
       int stage = 0;
       uint32_t phase = 0;
@@ -323,6 +391,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (kb == sg.kb0 && i == 0) HY_TR(4);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
@@ -337,6 +406,7 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
         umma_commit(&tfull[acc]);
+        if (i == 0) HY_TR(5);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -344,9 +414,10 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ---------------- epilogue warps 2..5 ----------------
+    // ---------------- epilogue warps 2..9 ----------------
     pdl_wait();  // residuals, partials and counters are written by earlier kernels
-    const int sub = warp & 3;  // TMEM lane sub-partition this warp may access
+    const int sub = warp & 3;          // TMEM lane sub-partition this warp may access
+    const int half = (warp - 2) >> 2;  // 32-column chunks half, half + 2, ...
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int i = 0; i < nseg; ++i) {
@@ -354,24 +425,26 @@ __global__ void __launch_bounds__(192, 1)
       int p, q;
       raster_tile(sg.tile, a, p, q);
       mbar_wait_sleepy(&tfull[acc], acc_phase);
+      if (i == 0 && threadIdx.x == 64) HY_TR(6);
       tc_fence_after();
       const int lrow = sub * 32 + lane;  // tile row (TMEM lane) owned by this thread
-      const int prow = p * 128 + lrow;
       const uint32_t taddr = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN;
       bool finish = true;
       int c0 = 0, c1 = -1;
       long long ub = 0;
       if (sg.slot >= 0) {
         // stream-K partial: publish raw accumulators, then count arrivals
-        float* mine = a.partial + ((size_t)(cta * 2 + sg.slot) * 128 + lrow) * BN;
+        // layout [cta][slot][chunk][j/4][128 rows] float4: lane-consecutive 16B stores
+        float4* mine = reinterpret_cast<float4*>(a.partial) +
+                       (size_t)(cta * 2 + sg.slot) * (BN / 32) * 8 * 128 + lrow;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = half; c < BN / 32; c += 2) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(taddr + c * 32, r);
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
-            __stcg(reinterpret_cast<float4*>(mine + c * 32 + j),
+            __stcg(mine + (c * 8 + j / 4) * 128,
                    make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
                                __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
         }
@@ -381,7 +454,7 @@ __global__ void __launch_bounds__(192, 1)
         __threadfence();
         __syncwarp();
         int prev = 0;
-        int* ctr = a.counters + sg.sk * 4 + sub;
+        int* ctr = a.counters + sg.sk * 8 + half * 4 + sub;
         if (lane == 0) prev = atomicAdd(ctr, 1);
         prev = __shfl_sync(0xffffffffu, prev, 0);
         finish = prev == c1 - c0;  // the last contributor reduces and writes the tile
@@ -392,50 +465,49 @@ __global__ void __launch_bounds__(192, 1)
       }
       if (finish) {
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = half; c < BN / 32; c += 2) {
           uint32_t r[32];
+          if (i == 0 && c == 0 && threadIdx.x == 64) HY_TR(9);
           tmem_ld_32x32b_x32(taddr + c * 32, r);
           tmem_ld_wait();
+          if (i == 0 && c == 0 && threadIdx.x == 64) HY_TR(10);
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
           // other contributors' partials (<= 3 by construction of the grid), all loads
           // issued before any add so the L2 round trips overlap
-          const float* srcs[3];
+          const float4* srcs[3];
           int ns = 0;
           for (int cc = c0; cc <= c1 && ns < 3; ++cc) {
             if (cc == cta) continue;
             const long long cu0 = (long long)cc * a.u_sk / G;
             const int slot = cu0 >= ub ? 0 : 1;
-            srcs[ns++] = a.partial + ((size_t)(cc * 2 + slot) * 128 + lrow) * BN + c * 32;
+            srcs[ns++] = reinterpret_cast<const float4*>(a.partial) +
+                         ((size_t)(cc * 2 + slot) * (BN / 32) + c) * 8 * 128 + lrow;
           }
-          float4 f[3][8];
+#pragma unroll 1
+          for (int s2 = 0; s2 < ns; ++s2) {
+            float4 f[8];
 #pragma unroll
-          for (int s2 = 0; s2 < 3; ++s2)
-            if (s2 < ns) {
+            for (int j = 0; j < 8; ++j) f[j] = __ldcg(srcs[s2] + j * 128);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) f[s2][j] = __ldcg(reinterpret_cast<const float4*>(srcs[s2]) + j);
+            for (int j = 0; j < 8; ++j) {
+              v[4 * j] += f[j].x;
+              v[4 * j + 1] += f[j].y;
+              v[4 * j + 2] += f[j].z;
+              v[4 * j + 3] += f[j].w;
             }
-#pragma unroll
-          for (int s2 = 0; s2 < 3; ++s2)
-            if (s2 < ns) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                v[4 * j] += f[s2][j].x;
-                v[4 * j + 1] += f[s2][j].y;
-                v[4 * j + 2] += f[s2][j].z;
-                v[4 * j + 3] += f[s2][j].w;
-              }
-            }
-          if (!SWAP)
-            epi_rows<EPI>(a, prow, q * BN + c * 32, v);
-          else
-            epi_cols<EPI>(a, prow, q * BN + c * 32, v, lane);
+          }
+          epi_chunk<EPI, SWAP>(a, p * 128 + sub * 32, q * BN + c * 32, v, lane,
+                               smem_u32(stg_base) + (warp - 2) * kStgBytes);
+          if (i == 0 && c == 0 && threadIdx.x == 64) HY_TR(11);
+          if (i == 0 && c == 1 && threadIdx.x == 64) HY_TR(12);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (i == 0 && threadIdx.x == 64) HY_TR(7);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -447,6 +519,223 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if (lane == 0) HY_TR(8);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1b: CTA-pair GEMM (tcgen05.mma.cta_group::2), normal orientation, pair tile 256 x BN.
+//
+// The two CTAs of a cluster sit on the two SMs of one TPC.  Each loads its own 128 token
+// rows of A and its own half (BN/2 rows) of the weight tile, so every byte staged in
+// shared memory feeds twice the MMA work of the single-CTA kernel (256 x BN x 64 per
+// stage pair) -- half the shared-memory traffic per flop, which is what lets the tensor
+// pipe run at full rate inside the power cap.  The leader CTA (rank 0) alone issues the
+// MMAs; both CTAs' TMA loads complete on the leader's full barrier, the MMA commits
+// multicast to both CTAs' empty / accumulator-full barriers, and both CTAs' epilogue warps
+// release the accumulator on the leader's accumulator-empty barrier.  Each CTA's TMEM
+// holds its own 128 rows of the 256 x BN accumulator (double-buffered).
+// ---------------------------------------------------------------------------
+template <int BN>
+struct GemmPairCfg {
+  static constexpr int BK = 64;
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int THREADS = 64 + 32 * kEpiWarps;
+};
+
+template <int BN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmArgs a) {
+  using C = GemmPairCfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::STAGES;
+  uint64_t* tfull = bars + 2 * C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+  const int T = a.np * a.nq;
+  pdl_trigger();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * kEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_cg2(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs) ----------------
+      const int rowA = rank * 128, rowB = rank * (BN / 2);
+      auto load_w = [&](int st, int kb, int q) {
+        if (rank == 0) mbar_expect_tx(&full[st], 2 * C::STAGE_BYTES);
+        tma_load_2d_cg2(&tmB, mapa_shared(smem_u32(&full[st]), 0), sB + st * C::B_BYTES,
+                        kb * C::BK, q * BN + rowB, kEvictNormal);
+      };
+      auto load_x = [&](int st, int kb, int p) {
+        tma_load_2d_cg2(&tmA, mapa_shared(smem_u32(&full[st]), 0), sA + st * C::A_BYTES,
+                        kb * C::BK, p * 256 + rowA, kEvictNormal);
+      };
+      // weights of the first stages before the grid dependency resolves
+      int npre = 0;
+      for (int t = pair; t < T && npre < C::STAGES; t += npairs) {
+        int p, q;
+        raster_tile(t, a, p, q);
+        for (int kb = 0; kb < a.nkb && npre < C::STAGES; ++kb, ++npre) load_w(npre, kb, q);
+      }
+      pdl_wait();
+      int stage = 0;
+      uint32_t phase = 0;
+      int g = 0;
+      for (int t = pair; t < T; t += npairs) {
+        int p, q;
+        raster_tile(t, a, p, q);
+        for (int kb = 0; kb < a.nkb; ++kb, ++g) {
+          if (g < npre) {
+            load_x(stage, kb, p);
+          } else {
+            mbar_wait(&empty[stage], phase ^ 1);
+            load_w(stage, kb, q);
+            load_x(stage, kb, p);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (leader CTA only) ----------------
+      constexpr uint32_t idesc = idesc_bf16_f32(256, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = pair; t < T; t += npairs) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < a.nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < C::BK / 16; ++k)
+            umma_bf16_cg2(d_tmem, smem_desc_k_sw128(a_addr + k * 32),
+                          smem_desc_k_sw128(b_addr + k * 32), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          umma_commit_cg2(&empty[stage], 0x3);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_cg2(&tfull[acc], 0x3);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..9 (both CTAs) ----------------
+    pdl_wait();
+    const int sub = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < T; t += npairs) {
+      int p, q;
+      raster_tile(t, a, p, q);
+      mbar_wait_sleepy(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = half; c < BN / 32; c += 2) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        epi_chunk<EPI, false>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32, v, lane, 0u);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no remote arrivals or pair MMAs in flight past this point
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_cg2(tmem_base, C::TMEM_COLS);
+  }
+}
+
+template <int BN, int EPI>
+static int launch_pair(const CUtensorMap& tA, const CUtensorMap& tB, const GemmArgs& a, int grid,
+                       cudaStream_t st) {
+  using C = GemmPairCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    HY_CUDA_RET(cudaFuncSetAttribute(gemm_pair_kernel<BN, EPI>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
+    attr_set = true;
+  }
+  HY_CUDA_RET(launch_pdl(gemm_pair_kernel<BN, EPI>, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES,
+                         st, tA, tB, a));
+  HY_LAUNCH_CHECK();
+  return 0;
+}
+
+static int launch_pair_epi(int epi, const CUtensorMap& tA, const CUtensorMap& tB,
+                           const GemmArgs& a, int grid, cudaStream_t st) {
+  switch (epi) {
+    case EPI_BF16: return launch_pair<256, EPI_BF16>(tA, tB, a, grid, st);
+    case EPI_QGELU: return launch_pair<256, EPI_QGELU>(tA, tB, a, grid, st);
+    case EPI_GELU: return launch_pair<256, EPI_GELU>(tA, tB, a, grid, st);
+    case EPI_SWIGLU: return launch_pair<256, EPI_SWIGLU>(tA, tB, a, grid, st);
+    case EPI_F32: return launch_pair<256, EPI_F32>(tA, tB, a, grid, st);
+    default: return -1;
   }
 }
 
@@ -493,6 +782,8 @@ static int launch_epi(int epi, int bn, const CUtensorMap& tA, const CUtensorMap&
 // Workspace layout: [counters: 16 KiB][partials: G * 2 * 128 * BN fp32].  The counter
 // region must be zero before first use; every call leaves it zeroed again.
 static constexpr size_t kCounterBytes = 16384;
+// token rows from which the CTA-pair kernel is used (tuned on B200, tools/kernel_sweep.py)
+static int kPairMinRows = 512;
 
 int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K,
               const HyGemmEpilogue* e, void* ws, size_t ws_bytes, cudaStream_t st, int force_mode) {
@@ -531,6 +822,25 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     HY_CHECK_ARG(false, "ldc must be a multiple of 8 for bf16 output");
   }
 
+  // CTA-pair kernel: large token counts, weight rows a multiple of 256
+  const bool pair = (force_mode == 3) ||
+                    (force_mode == 0 && M >= kPairMinRows && N % 256 == 0 && !getenv("HY_GEMM_NOPAIR"));
+  if (pair) {
+    a.np = ceil_div(M, 256);
+    a.nq = N / 256;
+    a.nkb = ceil_div(K, 64);
+    HY_CHECK_ARG(N % 256 == 0, "pair kernel needs N % 256 == 0");
+    const int grid = 2 * std::min(a.np * a.nq, num_sms() / 2);
+    CUtensorMap tA, tB;
+    HY_RET_IF(make_tmap_2d_bf16(&tA, A, M, K, (uint64_t)lda * 2, 128, 64));
+    HY_RET_IF(make_tmap_2d_bf16(&tB, W, N, K, (uint64_t)ldw * 2, 128, 64));
+    const int rc = launch_pair_epi(epi, tA, tB, a, grid, st);
+    if (rc < 0) {
+      set_last_error("gemm: no pair kernel for this epilogue");
+      return (int)cudaErrorInvalidValue;
+    }
+    return rc;
+  }
   const bool swap = (force_mode == 1) || (force_mode == 0 && M <= 256);
   int bn;
   if (swap) {

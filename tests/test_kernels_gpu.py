@@ -74,6 +74,14 @@ def _gemm_ref(A, W, bias, act, res):
     (1252, 2816, 512, 0, 4, False, False, False),     # prefill SwiGLU, normal mode
     (4096, 1024, 4096, 2, 0, True, True, False),
     (300, 512, 640, 0, 0, False, False, False),       # patch-embed K padding
+    # CTA-pair kernel (cta_group::2): ragged M, every epilogue, in-place residual shapes
+    (2304, 4096, 4096, 3, 0, False, True, False),
+    (577, 3072, 1024, 3, 0, True, False, False),
+    (1000, 4096, 1024, 3, 1, True, False, False),
+    (1252, 2816, 512, 3, 4, False, False, False),
+    (300, 1024, 1024, 3, 2, True, True, False),
+    (260, 32000, 512, 3, 0, False, False, True),
+    (4096, 12288, 4096, 0, 0, False, False, False),    # heuristic picks the pair kernel
 ])
 def test_gemm(M, N, K, mode, act, bias, res, f32):
     g = torch.Generator(device=DEV).manual_seed(M * 7 + N)

@@ -1,0 +1,155 @@
+"""Per-shape microbenchmarks of the serving kernels (LLaVA-1.5-7B shapes) on one B200.
+
+    python tools/kernel_sweep.py [--what gemm,attn,copy] [--json out.json]
+
+GEMM: hy_gemm_bf16 vs torch.matmul (cuBLAS) on the decoder / ViT / projector shapes
+the serving mix produces (decode M 1..256, mixed prefill M ~ tau_t, ViT M = 577 x images).
+Every timing: CUDA events on the launching stream, warm-up first, median of repeats,
+and the weights rotated through a set larger than L2 so each launch streams from HBM.
+Attention: decode (K8), paged prefill (K7), ViT varlen (K3) at serving shapes, reported
+as GB/s (decode) or TFLOP/s (4*d*keys per head).  Copy: hy_copy_blocks on 8 MiB KV blocks
+(same device; the peer-pointer path needs two GPUs).
+Never a source of bench numbers; it explains them.
+"""
+
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2505_12658_b200 import _lib  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def lib():
+    return _lib.load()
+
+
+def st():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def timeit(fn, reps=5, per_graph=20, warm=3):
+    """GPU time per launch: `per_graph` launches captured in one CUDA graph (no host
+    launch overhead in the measurement), replayed `reps` times, median."""
+    for i in range(warm):
+        fn(i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for i in range(per_graph):
+                fn(i)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    cur = torch.cuda.current_stream()
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        g.replay()
+        b.record(cur)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / per_graph)
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+VARIANTS = []
+ONLY = []
+EXTRA = []
+
+
+def gemm_sweep(out):
+    H, F, V = 4096, 11008, 32000
+    shapes = []
+    for M in (1, 16, 64, 128, 256, 512, 1024, 2304, 4096):
+        shapes += [("qkv", M, 3 * H, H), ("o", M, H, H), ("gate_up", M, 2 * F, H),
+                   ("down", M, H, F)]
+    shapes += [("lm_head", 64, V, H), ("lm_head", 256, V, H)]
+    for n_img in (1, 8, 56):
+        T = 577 * n_img
+        shapes += [("vit_qkv", T, 3072, 1024), ("vit_o", T, 1024, 1024),
+                   ("vit_fc1", T, 4096, 1024), ("vit_fc2", T, 1024, 4096),
+                   ("proj1", 576 * n_img, 4096, 1024), ("proj2", 576 * n_img, 4096, 4096)]
+    ws = torch.zeros(64 << 20, dtype=torch.uint8, device=DEV)
+    shapes += EXTRA
+    if ONLY:
+        shapes = [x for x in shapes if x[0] in ONLY]
+    for name, M, N, K in shapes:
+        nw = max(2, int(400e6 // (N * K * 2)) + 1)  # > L2 of weights in rotation
+        Ws = [torch.randn(N, K, device=DEV).mul_(0.02).bfloat16() for _ in range(nw)]
+        A = torch.randn(M, K, device=DEV).bfloat16()
+        C = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+        e = _lib.HyGemmEpilogue(0, 0, 0, 0, 0, C.data_ptr(), N, 0)
+
+        def ours(i):
+            W = Ws[i % nw]
+            rc = lib().hy_gemm_bf16(A.data_ptr(), K, W.data_ptr(), K, M, N, K, e,
+                                    ws.data_ptr(), ws.numel(), st())
+            assert rc == 0, lib().hy_last_error()
+
+        def cublas(i):
+            torch.matmul(A, Ws[i % nw].t(), out=C)
+
+        t0 = timeit(ours)
+        t1 = timeit(cublas)
+        var = {}
+        for v in VARIANTS:
+            old = {k: os.environ.get(k) for k in v}
+            os.environ.update(v)
+            try:
+                var[",".join(f"{k}={x}" for k, x in v.items())] = timeit(ours) * 1e3
+            except AssertionError:
+                pass
+            for k, x in old.items():
+                if x is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = x
+        fl = 2.0 * M * N * K
+        wb = N * K * 2 + M * K * 2 + M * N * 2
+        r = {"name": name, "M": M, "N": N, "K": K, "ours_us": t0 * 1e3, "cublas_us": t1 * 1e3,
+             "ours_tflops": fl / t0 / 1e9, "cublas_tflops": fl / t1 / 1e9,
+             "ours_gbs": wb / t0 / 1e6, "speedup_vs_cublas": t1 / t0, "variants_us": var}
+        out.append(r)
+        print(f"{name:8s} M={M:6d} N={N:6d} K={K:6d}  ours {t0*1e3:8.1f} us "
+              f"{r['ours_tflops']:7.1f} TF {r['ours_gbs']:7.0f} GB/s | cublas {t1*1e3:8.1f} us "
+              f"{r['cublas_tflops']:7.1f} TF | x{r['speedup_vs_cublas']:.2f} "
+              + " ".join(f"[{k}: {x:.1f}]" for k, x in var.items()), flush=True)
+        del Ws
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--what", default="gemm")
+    ap.add_argument("--json", default=None)
+    ap.add_argument("--variants", default="",
+                    help="';'-separated env settings, e.g. 'HY_GEMM_NOSK=1;HY_GEMM_BN=128'")
+    ap.add_argument("--only", default="", help="comma list of shape names")
+    ap.add_argument("--shapes", default="", help="extra MxNxK list, e.g. 128x128x64,577x1024x1024")
+    args = ap.parse_args()
+    for v in filter(None, args.variants.split(";")):
+        VARIANTS.append(dict(kv.split("=") for kv in v.split(",")))
+    ONLY.extend(filter(None, args.only.split(",")))
+    for x in filter(None, args.shapes.split(",")):
+        M, N, K = (int(v) for v in x.split("x"))
+        EXTRA.append(("custom", M, N, K))
+    res = {}
+    if "gemm" in args.what:
+        res["gemm"] = []
+        gemm_sweep(res["gemm"])
+    if args.json:
+        with open(args.json, "w") as fh:
+            json.dump(res, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
