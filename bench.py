@@ -68,6 +68,10 @@ def parse():
 
 
 # ----------------------------------------------------------------------------- helpers
+def log(msg):
+    print(f"[bench] {msg}", file=sys.stderr, flush=True)
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -231,6 +235,7 @@ def run_ours(args, d: Dist):
     for i in range(args.warmup):
         replay(50.0 * (i + 1), trace=warm)[0].close()
     torch.cuda.synchronize()
+    log(f"warm-up done; budgets {budgets_seen}")
 
     # ---- timed goodput search: K probes
     probe_info = []
@@ -265,6 +270,8 @@ def run_ours(args, d: Dist):
                            "ttft_p90": a["ttft_percentiles_s"].get("p90"),
                            "tbt_p90": a["tbt_percentiles_s"].get("p90")})
         cl.close()
+        log(f"probe rate {total:.1f}: attainment {att:.3f}, {int(tot[5])} batches, "
+            f"wall {span[1]:.1f} s")
         return att
 
     best, probes = geometric_bisect(probe, args.rate_lo, args.rate_hi, args.steps)
@@ -292,7 +299,7 @@ def run_ours(args, d: Dist):
                     "peak_source": f"{peak_src} hbm_gbs"}
         ach = s["work_per_ms"] / 1e9  # flop/ms -> TFLOP/s
         pk = peaks["bf16_tflops_sustained"]
-        return {"kernel": {"gemm": "gemm_tc_kernel (K1, tcgen05)",
+        return {"kernel": {"gemm": "gemm_tc_kernel + gemm_pair_kernel (K1, tcgen05)",
                            "prefill_attn": "attn_fa2_kernel<128,paged> (K7)",
                            "vit_attn": "attn_fa2_kernel<64> (K3)"}[name],
                 "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
@@ -323,6 +330,7 @@ def run_ours(args, d: Dist):
             tot = d.reduce([meets, len(rep.requests)])
             att = tot[0] / tot[1]
             e2e_probes.append((r * d.world, att))
+            log(f"e2e probe rate {r * d.world:.1f}: attainment {att:.3f}")
             n_img = sum(rt.stats["images"] for rt in cl.runtimes.values())
             n_tok = sum(r_.tokens_out for r_ in cl.reqs.values())
             cl.close()

@@ -58,6 +58,7 @@ struct GemmArgs {
   int P, Q, K;    // MMA-M extent (rows of map A), MMA-N extent (rows of map B), reduction
   int np, nq, nkb;
   int t_dp;       // whole tiles [0, t_dp) round-robin (multiple of the grid when stream-K)
+  int dbg;        // pair kernel PDL bits (HY_PAIR_DBG): 1 no early trigger, 2 no PDL launch
   long long u_sk; // k-block units of tiles [t_dp, T), split evenly over the grid
   int M, N;       // logical GEMM shape (tokens, physical weight rows)
   const bf16* bias;
@@ -572,7 +573,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
   const int T = a.np * a.nq;
-  pdl_trigger();
+  if (!(a.dbg & 1)) pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -721,8 +722,11 @@ static int launch_pair(const CUtensorMap& tA, const CUtensorMap& tB, const GemmA
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
     attr_set = true;
   }
-  HY_CUDA_RET(launch_pdl(gemm_pair_kernel<BN, EPI>, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES,
-                         st, tA, tB, a));
+  if (a.dbg & 2)
+    gemm_pair_kernel<BN, EPI><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tA, tB, a);
+  else
+    HY_CUDA_RET(launch_pdl(gemm_pair_kernel<BN, EPI>, dim3(grid), dim3(C::THREADS),
+                           C::SMEM_BYTES, st, tA, tB, a));
   HY_LAUNCH_CHECK();
   return 0;
 }
@@ -783,7 +787,7 @@ static int launch_epi(int epi, int bn, const CUtensorMap& tA, const CUtensorMap&
 // region must be zero before first use; every call leaves it zeroed again.
 static constexpr size_t kCounterBytes = 16384;
 // token rows from which the CTA-pair kernel is used (tuned on B200, tools/kernel_sweep.py)
-static int kPairMinRows = 512;
+static constexpr int kPairMinRows = 512;
 
 int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K,
               const HyGemmEpilogue* e, void* ws, size_t ws_bytes, cudaStream_t st, int force_mode) {
@@ -823,14 +827,26 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   }
 
   // CTA-pair kernel: large token counts, weight rows a multiple of 256
-  const bool pair = (force_mode == 3) ||
-                    (force_mode == 0 && M >= kPairMinRows && N % 256 == 0 && !getenv("HY_GEMM_NOPAIR"));
+  // when it needs no more full waves than the single-CTA kernel (a pair tile takes about as
+  // long on two SMs as a 128-row tile on one, so waves decide)
+  bool pair = force_mode == 3;
+  if (force_mode == 0 && M >= kPairMinRows && N % 256 == 0 && !getenv("HY_GEMM_NOPAIR")) {
+    const int sms = num_sms();
+    const int waves_pair = ceil_div(ceil_div(M, 256) * (N / 256), sms / 2);
+    const int waves_single = ceil_div(ceil_div(M, 128) * (N / 256), sms);
+    pair = waves_pair <= waves_single;
+  }
   if (pair) {
     a.np = ceil_div(M, 256);
     a.nq = N / 256;
     a.nkb = ceil_div(K, 64);
     HY_CHECK_ARG(N % 256 == 0, "pair kernel needs N % 256 == 0");
     const int grid = 2 * std::min(a.np * a.nq, num_sms() / 2);
+    // The pair kernel does not release its dependents early: with an early trigger, a
+    // PDL-launched pair GEMM plus early-launched dependents hung the serving replay on B200
+    // (bisected with HY_PAIR_DBG: trigger off or PDL launch off both run clean).
+    a.dbg = 1;
+    if (const char* d = getenv("HY_PAIR_DBG")) a.dbg = atoi(d);
     CUtensorMap tA, tB;
     HY_RET_IF(make_tmap_2d_bf16(&tA, A, M, K, (uint64_t)lda * 2, 128, 64));
     HY_RET_IF(make_tmap_2d_bf16(&tB, W, N, K, (uint64_t)ldw * 2, 128, 64));

@@ -376,8 +376,15 @@ class InstanceRuntime:
         host_s = time.perf_counter() - t_host0
         if sampler is not None:
             ctx_sum = sum(kl + 1 for _, kl in batch.decode_entries)
-            sampler.after_batch(dev_ms, ctx_sum * self.shape.kv_bytes_per_token /
-                                self.shape.n_layers)
+            s = self.shape
+            keys = sum(c * reqs[rid].prefill_done + c * (c + 1) // 2
+                       for rid, c in batch.prefill_chunks)
+            vit_sq = sum(s.vit_tokens(T) ** 2 for rid, k, counts in batch.encode_entries
+                         for T in reqs[rid].spec.image_token_counts[
+                             reqs[rid].images_done:reqs[rid].images_done + k])
+            sampler.after_batch(dev_ms, ctx_sum * s.kv_bytes_per_token / s.n_layers,
+                                4.0 * s.head_dim * s.n_heads * keys,
+                                4.0 * s.v_head_dim * s.v_heads * vit_sq)
         self.stats["batches"] += 1
         if self.capture:
             entry = {

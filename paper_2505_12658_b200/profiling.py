@@ -10,6 +10,9 @@ Algorithmic work per launch:
   decode attn    bytes = sum_i ctx_i * kv_bytes_per_token_per_layer (K+V of every key
                  read once; epdsim charges 2*B*H*(S+1)*ratio per layer,
                  model_cost.py:195) -- filled in here from the batch
+  prefill attn   flops = 4 * d * heads * sum over chunk queries of keys attended (causal,
+                 offset by the chunk start)
+  ViT attn       flops = 4 * d * heads * sum over images of tokens^2 (block-diagonal)
 """
 
 from __future__ import annotations
@@ -59,8 +62,10 @@ class KernelSampler:
         self.timer.count = 0
         self.lib.hy_set_kernel_timer(ctypes.byref(self.timer))
 
-    def after_batch(self, batch_device_ms: float, decode_ctx_bytes: float) -> None:
-        """Call after the batch completed (events are final)."""
+    def after_batch(self, batch_device_ms: float, decode_ctx_bytes: float,
+                    prefill_attn_flops: float = 0.0, vit_attn_flops: float = 0.0) -> None:
+        """Call after the batch completed (events are final).  The attention works are per
+        layer launch (bytes for decode, flops for prefill / ViT attention)."""
         if self.active is None:
             return
         self.lib.hy_set_kernel_timer(None)
@@ -71,6 +76,10 @@ class KernelSampler:
             work = self._work[i]
             if name == "decode_attn":
                 work = decode_ctx_bytes
+            elif name == "prefill_attn":
+                work = prefill_attn_flops
+            elif name == "vit_attn":
+                work = vit_attn_flops
             self.samples[name].append((ms, work))
             tot += ms
         self.batch_ms[name] += batch_device_ms

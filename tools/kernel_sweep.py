@@ -70,11 +70,11 @@ EXTRA = []
 def gemm_sweep(out):
     H, F, V = 4096, 11008, 32000
     shapes = []
-    for M in (1, 16, 64, 128, 256, 512, 1024, 2304, 4096):
+    for M in (1, 16, 64, 128, 256, 512, 1024, 1600, 2304, 4096):
         shapes += [("qkv", M, 3 * H, H), ("o", M, H, H), ("gate_up", M, 2 * F, H),
                    ("down", M, H, F)]
     shapes += [("lm_head", 64, V, H), ("lm_head", 256, V, H)]
-    for n_img in (1, 8, 56):
+    for n_img in (1, 2, 3, 8, 56):
         T = 577 * n_img
         shapes += [("vit_qkv", T, 3072, 1024), ("vit_o", T, 1024, 1024),
                    ("vit_fc1", T, 4096, 1024), ("vit_fc2", T, 1024, 4096),
@@ -127,6 +127,83 @@ def gemm_sweep(out):
         del Ws
 
 
+def attn_sweep(out):
+    """ViT varlen (K3) and paged prefill (K7) attention vs flash_attn (library, reference
+    speed only -- never on the product path)."""
+    import math
+    import numpy as np
+    try:
+        from flash_attn import flash_attn_varlen_func
+    except Exception:  # noqa: BLE001
+        flash_attn_varlen_func = None
+    # ViT: n images x 577 tokens, 16 heads x 64
+    for n_img in (1, 3, 8, 32):
+        nh, d, T = 16, 64, 577
+        tot = n_img * T
+        qkv = torch.randn(tot, 3 * nh * d, device=DEV).bfloat16()
+        o = torch.empty(tot, nh * d, device=DEV, dtype=torch.bfloat16)
+        seg = torch.arange(0, tot + 1, T, dtype=torch.int32, device=DEV)
+
+        def ours(i):
+            rc = lib().hy_attn_varlen(qkv.data_ptr(), 3 * nh * d, n_img, seg.data_ptr(), T, nh, d,
+                                      1 / math.sqrt(d), o.data_ptr(), nh * d, st())
+            assert rc == 0, lib().hy_last_error()
+        t0 = timeit(ours)
+        t1 = None
+        if flash_attn_varlen_func is not None:
+            q3 = qkv.view(tot, 3, nh, d)
+            q, k, v = q3[:, 0], q3[:, 1], q3[:, 2]
+
+            def fa(i):
+                flash_attn_varlen_func(q, k, v, seg, seg, T, T)
+            t1 = timeit(fa)
+        fl = 4.0 * d * nh * n_img * T * T
+        r = {"name": "vit_attn", "images": n_img, "ours_us": t0 * 1e3,
+             "ours_tflops": fl / t0 / 1e9, "fa_us": t1 * 1e3 if t1 else None,
+             "fa_tflops": fl / t1 / 1e9 if t1 else None}
+        out.append(r)
+        print(f"vit_attn images={n_img:3d}  ours {t0*1e3:8.1f} us {r['ours_tflops']:7.1f} TF | "
+              f"flash_attn {r['fa_us'] or 0:8.1f} us {r['fa_tflops'] or 0:7.1f} TF", flush=True)
+    # prefill: chunks (offset, len) over paged KV, 32 heads x 128
+    for chunks in ([(0, 616)], [(0, 616)] * 4, [(0, 1024), (1024, 1024)], [(0, 2304)]):
+        nh, d = 32, 128
+        n = len(chunks)
+        ctxs = [a + b for a, b in chunks]
+        nblk = [-(-c // 16) for c in ctxs]
+        block_elems = 2 * nh * 16 * d
+        kv = torch.randn(sum(nblk) + 1, block_elems, device=DEV).bfloat16()
+        bts = max(nblk)
+        bt = torch.zeros(n, bts, dtype=torch.int32)
+        u = 0
+        for i, nb in enumerate(nblk):
+            bt[i, :nb] = torch.arange(u, u + nb, dtype=torch.int32)
+            u += nb
+        bt = bt.to(DEV)
+        rows = sum(c for _, c in chunks)
+        q = torch.randn(rows, nh * d, device=DEV).bfloat16()
+        o = torch.empty_like(q)
+        qstart = torch.tensor(np.cumsum([0] + [c for _, c in chunks]), dtype=torch.int32,
+                              device=DEV)
+        offs = torch.tensor([a for a, _ in chunks], dtype=torch.int32, device=DEV)
+        slots = torch.arange(n, dtype=torch.int32, device=DEV)
+        mq = max(c for _, c in chunks)
+
+        def ours(i):
+            rc = lib().hy_attn_prefill_paged(q.data_ptr(), nh * d, n, qstart.data_ptr(),
+                                             offs.data_ptr(), slots.data_ptr(), mq, nh, nh, d,
+                                             bt.data_ptr(), bts, kv.data_ptr(), block_elems,
+                                             1 / math.sqrt(d), o.data_ptr(), nh * d, st())
+            assert rc == 0, lib().hy_last_error()
+        t0 = timeit(ours)
+        keys = sum(c * a + c * (c + 1) // 2 for a, c in chunks)
+        fl = 4.0 * d * nh * keys
+        r = {"name": "prefill_attn", "chunks": chunks, "ours_us": t0 * 1e3,
+             "ours_tflops": fl / t0 / 1e9}
+        out.append(r)
+        print(f"prefill_attn {chunks}  ours {t0*1e3:8.1f} us {r['ours_tflops']:7.1f} TF",
+              flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--what", default="gemm")
@@ -146,6 +223,9 @@ def main():
     if "gemm" in args.what:
         res["gemm"] = []
         gemm_sweep(res["gemm"])
+    if "attn" in args.what:
+        res["attn"] = []
+        attn_sweep(res["attn"])
     if args.json:
         with open(args.json, "w") as fh:
             json.dump(res, fh, indent=1)

@@ -20,7 +20,13 @@ def main():
     ap.add_argument("--requests", type=int, default=48)
     ap.add_argument("--rate", type=float, default=60.0)
     ap.add_argument("--model", default="llava-1.5-7b")
+    ap.add_argument("--budgets", default="roofline", choices=["roofline", "measured"])
+    ap.add_argument("--watchdog", type=float, default=0.0,
+                    help="dump Python stacks and exit after this many seconds (hang triage)")
     args = ap.parse_args()
+    if args.watchdog:
+        import faulthandler
+        faulthandler.dump_traceback_later(args.watchdog, exit=True)
     import torch
     import paper_2505_12658_b200 as P
     from paper_2505_12658_b200._epdsim import C, E
@@ -31,7 +37,8 @@ def main():
                        visual_token_choices=576, prompt_dist=[25, 35, 45],
                        output_dist=[90, 110, 130], slo=slo)
     spec = C.ClusterSpec(method=C.DisaggregationMethod.parse("EPD:1"))
-    cl = GpuCluster(spec, shape, P.b200_hardware(), slo, clock="device")
+    cl = GpuCluster(spec, shape, P.b200_hardware(), slo, clock="device",
+                    budgets=args.budgets)
     rep = cl.run(tr)
     torch.cuda.synchronize()
     rt = next(iter(cl.runtimes.values()))
