@@ -267,6 +267,10 @@ def run_ours(args, d: Dist):
                            "virtual_span_s": span[0], "tokens": tot[3],
                            "decode_tok_s": tot[3] / span[0] if span[0] > 0 else 0.0,
                            "device_busy_s": tot[4] / 1e3, "batches": int(tot[5]),
+                           "vision_critical": [sum(rt.stats["vision_critical"]
+                                                   for rt in cl.runtimes.values()),
+                                               sum(rt.stats["mixed_batches"]
+                                                   for rt in cl.runtimes.values())],
                            "ttft_p90": a["ttft_percentiles_s"].get("p90"),
                            "tbt_p90": a["tbt_percentiles_s"].get("p90")})
         cl.close()
@@ -315,6 +319,8 @@ def run_ours(args, d: Dist):
             return None
 
     roofline = roof(dominant) if dominant else None
+    if roofline is not None and dominant == "gemm":
+        roofline["by_shape"] = sampler.gemm_breakdown()
     others = {k: roof(k) for k in summ if k != dominant}
 
     # ---- end-to-end through host buffers (wall clock per batch)

@@ -86,6 +86,7 @@ typedef struct HyKernelTimer {
   int count;
   void* events;  /* cudaEvent_t[2 * capacity] */
   double* work;  /* [capacity] or NULL */
+  long long* shape; /* [capacity] or NULL: GEMM (M << 42) | (N << 21) | K */
 } HyKernelTimer;
 void hy_set_kernel_timer(HyKernelTimer* timer);
 

@@ -85,7 +85,7 @@ class HyVitModel(Structure):
 
 class HyKernelTimer(Structure):
     _fields_ = [("klass", c_int), ("capacity", c_int), ("count", c_int), ("events", c_void_p),
-                ("work", c_void_p)]
+                ("work", c_void_p), ("shape", c_void_p)]
 
 
 HY_KCLASS_DECODE_ATTN = 1

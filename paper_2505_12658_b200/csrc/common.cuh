@@ -355,7 +355,7 @@ int make_tmap_2d_bf16(CUtensorMap* tm, const void* base, uint64_t rows, uint64_t
 int num_sms();
 
 // kernel-class timer hooks (see hy_set_kernel_timer)
-void timer_mark(int klass, cudaStream_t st, bool begin, double work);
+void timer_mark(int klass, cudaStream_t st, bool begin, double work, long long shape = 0);
 
 // ---------------------------------------------------------------------------
 // Programmatic dependent launch.  Every kernel of the serving path is launched with

@@ -109,7 +109,8 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
     timer_mark(HY_KCLASS_GEMM, st, true, 0.0);
     int rc = gemm_bf16(A, lda, reinterpret_cast<const bf16*>(W), K, M, N, K, &e, w.gemm_ws,
                        kGemmWs, st, 0);
-    timer_mark(HY_KCLASS_GEMM, st, false, 2.0 * M * N * K);
+    timer_mark(HY_KCLASS_GEMM, st, false, 2.0 * M * N * K,
+               ((long long)M << 42) | ((long long)N << 21) | (long long)K);
     return rc;
   };
   const float scale = 1.0f / sqrtf((float)D);
@@ -217,7 +218,8 @@ extern "C" int hy_vit_forward(const HyVitModel* m, const HyVitBatch* b, void* wo
     timer_mark(HY_KCLASS_GEMM, st, true, 0.0);
     int rc = gemm_bf16(A, lda, reinterpret_cast<const bf16*>(W), K, M, N, K, &e, w.gemm_ws,
                        kGemmWs, st, 0);
-    timer_mark(HY_KCLASS_GEMM, st, false, 2.0 * M * N * K);
+    timer_mark(HY_KCLASS_GEMM, st, false, 2.0 * M * N * K,
+               ((long long)M << 42) | ((long long)N << 21) | (long long)K);
     return rc;
   };
   // K2: patch embedding

@@ -93,7 +93,7 @@ extern "C" long long hy_launch_count(void) { return hy::g_launches.load(); }
 // ---------------------------------------------------------------------------
 namespace hy {
 static HyKernelTimer* g_timer = nullptr;
-void timer_mark(int klass, cudaStream_t st, bool begin, double work) {
+void timer_mark(int klass, cudaStream_t st, bool begin, double work, long long shape) {
   HyKernelTimer* t = g_timer;
   if (!t || t->klass != klass) return;
   if (t->count >= t->capacity) return;
@@ -101,6 +101,7 @@ void timer_mark(int klass, cudaStream_t st, bool begin, double work) {
   cudaEventRecord(reinterpret_cast<cudaEvent_t*>(t->events)[slot], st);
   if (!begin) {
     if (t->work) t->work[t->count] = work;
+    if (t->shape) t->shape[t->count] = shape;
     t->count++;
   }
 }

@@ -27,6 +27,7 @@ It never mutates ``batch`` or ``reqs`` (the loop does that in ``_on_batch_done``
 from __future__ import annotations
 
 import itertools
+import os
 import time
 from typing import Dict, List, Optional, Tuple
 
@@ -98,8 +99,12 @@ class InstanceRuntime:
             self.block_table = torch.zeros((max_slots, self.bt_stride), dtype=torch.int32,
                                            device=self.device)
             self.last_tok = torch.zeros(max_slots, dtype=torch.int32, device=self.device)
-            self.stream_l = torch.cuda.Stream(self.device)
-            self.stream_v = torch.cuda.Stream(self.device)
+            # the vision tower is the small side of a mixed batch: give its stream the higher
+            # priority so its CTAs are scheduled as soon as language-GEMM CTAs retire instead
+            # of stretching over the whole batch (HY_VSTREAM_PRIO=0 disables)
+            hi = os.environ.get("HY_VSTREAM_PRIO", "1") != "0"
+            self.stream_l = torch.cuda.Stream(self.device, priority=0)
+            self.stream_v = torch.cuda.Stream(self.device, priority=-1 if hi else 0)
             self.ev_start = torch.cuda.Event(enable_timing=True)
             self.ev_l = torch.cuda.Event(enable_timing=True)
             self.ev_v = torch.cuda.Event(enable_timing=True)
@@ -131,7 +136,8 @@ class InstanceRuntime:
         self.exec_log: List[Dict] = []
         self.sampler = None  # profiling.KernelSampler (bench.py)
         self.stats = {"batches": 0, "lang_rows": 0, "decode_rows": 0, "prefill_rows": 0,
-                      "images": 0, "device_ms": 0.0, "host_ms": 0.0}
+                      "images": 0, "device_ms": 0.0, "host_ms": 0.0, "mixed_batches": 0,
+                      "vision_critical": 0}
 
     # ------------------------------------------------------------------ helpers
     def prompt(self, r) -> np.ndarray:
@@ -371,8 +377,12 @@ class InstanceRuntime:
                 host.copy_(self.tok_log[tok_off:tok_off + n_out], non_blocking=True)
         self.ev_v.synchronize()
         self.ev_l.synchronize()
-        dev_ms = max(self.ev_start.elapsed_time(self.ev_l),
-                     self.ev_start.elapsed_time(self.ev_v) if has_vis else 0.0)
+        t_l = self.ev_start.elapsed_time(self.ev_l)
+        t_v = self.ev_start.elapsed_time(self.ev_v) if has_vis else 0.0
+        dev_ms = max(t_l, t_v)
+        if has_vis and has_lang:
+            self.stats["mixed_batches"] += 1
+            self.stats["vision_critical"] += int(t_v > t_l)
         host_s = time.perf_counter() - t_host0
         if sampler is not None:
             ctx_sum = sum(kl + 1 for _, kl in batch.decode_entries)

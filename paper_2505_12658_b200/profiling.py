@@ -41,8 +41,11 @@ class KernelSampler:
             s.synchronize()
         self._handles = (ctypes.c_void_p * (2 * capacity))(*[e.cuda_event for e in self.events])
         self._work = (ctypes.c_double * capacity)()
+        self._shape = (ctypes.c_longlong * capacity)()
         self.timer = _lib.HyKernelTimer(0, capacity, 0, ctypes.addressof(self._handles),
-                                        ctypes.addressof(self._work))
+                                        ctypes.addressof(self._work),
+                                        ctypes.addressof(self._shape))
+        self.gemm_shapes: Dict[tuple, List[float]] = {}  # (M bin, N, K) -> [ms, flops, n]
         self.n_batches = 0
         self.active = None
         # per class: list of (ms, work) per launch; plus sampled batch device time
@@ -82,9 +85,25 @@ class KernelSampler:
                 work = vit_attn_flops
             self.samples[name].append((ms, work))
             tot += ms
+            if name == "gemm" and self._shape[i]:
+                sh = self._shape[i]
+                M, N, K = sh >> 42, (sh >> 21) & 0x1FFFFF, sh & 0x1FFFFF
+                mb = 1 << max(0, (M - 1).bit_length())  # power-of-two bin
+                acc = self.gemm_shapes.setdefault((mb, N, K), [0.0, 0.0, 0])
+                acc[0] += ms
+                acc[1] += work
+                acc[2] += 1
         self.batch_ms[name] += batch_device_ms
         self.class_ms[name] += tot
         self.active = None
+
+    def gemm_breakdown(self, top: int = 16) -> List[Dict]:
+        """GEMM time by (M rounded up to a power of two, N, K), largest share first."""
+        tot = sum(v[0] for v in self.gemm_shapes.values()) or 1.0
+        rows = [{"M_bin": k[0], "N": k[1], "K": k[2], "share": v[0] / tot,
+                 "tflops": v[1] / v[0] / 1e9 if v[0] > 0 else 0.0, "launches": v[2]}
+                for k, v in self.gemm_shapes.items()]
+        return sorted(rows, key=lambda r: -r["share"])[:top]
 
     def summary(self) -> Dict[str, Dict]:
         out = {}

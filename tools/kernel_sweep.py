@@ -204,6 +204,73 @@ def attn_sweep(out):
               flush=True)
 
 
+def overlap_probe(out):
+    """Can HBM-bound decode attention overlap tensor-bound prefill GEMMs on separate
+    streams?  Times each alone and both concurrently (decode attention of 256 sequences x
+    660 context, LLaVA 32x128 heads; gate_up GEMM 2304 x 22016 x 4096)."""
+    import math
+    n, ctx, nh, d = 256, 660, 32, 128
+    nb = -(-ctx // 16)
+    block_elems = 2 * nh * 16 * d  # one layer
+    kv = torch.randn(n * nb + 1, block_elems, device=DEV).bfloat16()
+    bt = torch.arange(n * nb, dtype=torch.int32, device=DEV).view(n, nb).contiguous()
+    q = torch.randn(n, nh * d, device=DEV).bfloat16()
+    o = torch.empty_like(q)
+    slots = torch.arange(n, dtype=torch.int32, device=DEV)
+    ctxs = torch.full((n,), ctx, dtype=torch.int32, device=DEV)
+    wsb = lib().hy_attn_decode_workspace_bytes(n, nh, d, ctx)
+    dws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=DEV)
+    M, N, K = 2304, 22016, 4096
+    A = torch.randn(M, K, device=DEV).bfloat16()
+    W = (torch.randn(N, K, device=DEV) * 0.02).bfloat16()
+    C = torch.empty(M, N // 2, device=DEV, dtype=torch.bfloat16)
+    gws = torch.zeros(64 << 20, dtype=torch.uint8, device=DEV)
+    e = _lib.HyGemmEpilogue(0, 0, 0, _lib.HY_ACT_SWIGLU, 0, C.data_ptr(), N // 2, 0)
+    s_att = torch.cuda.Stream(priority=-1)
+    s_gemm = torch.cuda.Stream()
+
+    def att(stream):
+        rc = lib().hy_attn_decode_paged(q.data_ptr(), nh * d, n, nh, nh, d, slots.data_ptr(),
+                                        ctxs.data_ptr(), ctx, bt.data_ptr(), nb, kv.data_ptr(),
+                                        block_elems, 1 / math.sqrt(d), o.data_ptr(), nh * d,
+                                        dws.data_ptr(), dws.numel(), stream.cuda_stream)
+        assert rc == 0, lib().hy_last_error()
+
+    def gemm(stream):
+        rc = lib().hy_gemm_bf16(A.data_ptr(), K, W.data_ptr(), K, M, N, K, e, gws.data_ptr(),
+                                gws.numel(), stream.cuda_stream)
+        assert rc == 0, lib().hy_last_error()
+
+    def run(which, reps=20):
+        torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream()
+        ev0.record(cur)
+        s_att.wait_stream(cur)
+        s_gemm.wait_stream(cur)
+        for _ in range(reps):
+            if "a" in which:
+                att(s_att)
+            if "g" in which:
+                gemm(s_gemm)
+        cur.wait_stream(s_att)
+        cur.wait_stream(s_gemm)
+        ev1.record(cur)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) / reps
+
+    for w in ("a", "g", "ag"):
+        run(w, 3)
+    ta, tg, tb = run("a"), run("g"), run("ag")
+    r = {"name": "overlap", "attn_ms": ta, "gemm_ms": tg, "both_ms": tb,
+         "sum_ms": ta + tg, "max_ms": max(ta, tg)}
+    out.append(r)
+    print(f"overlap: attn {ta:.3f} ms ({n * ctx * block_elems * 2 / ta / 1e9:.0f} GB/s), "
+          f"gemm {tg:.3f} ms, concurrent {tb:.3f} ms (sum {ta + tg:.3f}, max {max(ta, tg):.3f})",
+          flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--what", default="gemm")
@@ -226,6 +293,9 @@ def main():
     if "attn" in args.what:
         res["attn"] = []
         attn_sweep(res["attn"])
+    if "overlap" in args.what:
+        res["overlap"] = []
+        overlap_probe(res["overlap"])
     if args.json:
         with open(args.json, "w") as fh:
             json.dump(res, fh, indent=1)
