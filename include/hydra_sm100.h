@@ -138,16 +138,18 @@ size_t hy_attn_decode_workspace_bytes(int n, int n_heads, int head_dim, int max_
 
 /* ---------------- K7: paged prefill attention (causal with offset) ---------------- */
 /* sequence s owns query rows [qstart[s], qstart[s+1]) at positions offset[s] + i and
- * attends to keys [0, offset[s] + i] of slot slots[s] in the paged cache. */
-int hy_attn_prefill_paged(const void* q, int ld_q, int n_seqs, const int* qstart,
+ * attends to keys [0, offset[s] + i] of slot slots[s] in the paged cache.  n_rows: rows of
+ * the q buffer (qstart[n_seqs]).  head_dim 64/128 runs on tcgen05 (attn_tc.cu). */
+int hy_attn_prefill_paged(const void* q, int ld_q, int n_rows, int n_seqs, const int* qstart,
                           const int* offset, const int* slots, int max_q, int n_heads,
                           int n_kv_heads, int head_dim, const int* block_table, int bt_stride,
                           const void* kv_layer, long long block_stride, float scale, void* out,
                           int ld_o, cudaStream_t stream);
 
 /* ---------------- K3: ViT varlen attention (block-diagonal, non-causal) ---------------- */
-/* qkv rows [q | k | v] (n_heads x d each); segment s = rows [seg[s], seg[s+1]). */
-int hy_attn_varlen(const void* qkv, int ld_qkv, int n_segs, const int* seg, int max_len,
+/* qkv rows [q | k | v] (n_heads x d each); segment s = rows [seg[s], seg[s+1]);
+ * n_rows = seg[n_segs].  head_dim 64/128 runs on tcgen05 (attn_tc.cu). */
+int hy_attn_varlen(const void* qkv, int ld_qkv, int n_rows, int n_segs, const int* seg, int max_len,
                    int n_heads, int head_dim, float scale, void* out, int ld_o,
                    cudaStream_t stream);
 

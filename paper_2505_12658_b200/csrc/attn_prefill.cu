@@ -1,11 +1,10 @@
 // K7 paged prefill attention (causal with a chunk offset) and K3 ViT varlen attention
 // (block-diagonal, non-causal), one flash-attention kernel templated on the KV source.
 //
-// Round-1 implementation: FA2-style tiling on the warp-level tensor-core path
-// (mma.sync m16n8k16 bf16 -> fp32) with cp.async double-buffered K/V tiles.  Attention
-// is ~1-4% of the LLaVA-1.5-7B prefill / ViT FLOPs (577-token images, 616-token prompts),
-// so the tcgen05 rewrite is scheduled after the GEMM and decode kernels reach roofline
-// ("next").
+// This file: the FA2-style kernel on the warp-level tensor-core path (mma.sync m16n8k16
+// bf16 -> fp32, cp.async double-buffered K/V) for head sizes the tcgen05 kernel does not
+// take (Qwen2-VL vision d = 80), and the C-ABI entry points, which dispatch d = 64 / 128 to
+// the tcgen05 + TMEM kernel in attn_tc.cu.
 //
 // Work per CTA: 64 query rows of one (sequence, head); 4 warps x 16 rows.  K/V tiles of
 // 64 keys; paged tiles are 4 consecutive 16-token blocks read through the block table.
@@ -264,17 +263,36 @@ static int launch_fa(const FaParams& p, int n_seqs, int n_heads, cudaStream_t st
   return 0;
 }
 
+int attn_tc_prefill(const void* q, int ld_q, int n_rows, int n_seqs, const int* qstart,
+                    const int* offset, const int* slots, int max_q, int n_heads, int n_kv_heads,
+                    int head_dim, const int* block_table, int bt_stride, const void* kv_layer,
+                    long long block_stride, float scale, void* out, int ld_o, cudaStream_t st);
+int attn_tc_varlen(const void* qkv, int ld_qkv, int n_rows, int n_segs, const int* seg,
+                   int max_len, int n_heads, int head_dim, float scale, void* out, int ld_o,
+                   cudaStream_t st);
+
+// tcgen05 kernel for head_dim 64/128 unless HY_ATTN_FA2 is set (A/B measurement only)
+static bool use_tc(int head_dim) {
+  static const bool fa2 = getenv("HY_ATTN_FA2") != nullptr;
+  return !fa2 && (head_dim == 64 || head_dim == 128);
+}
+
 }  // namespace hy
 
 using namespace hy;
 
-extern "C" int hy_attn_prefill_paged(const void* q, int ld_q, int n_seqs, const int* qstart,
-                                     const int* offset, const int* slots, int max_q, int n_heads,
-                                     int n_kv_heads, int head_dim, const int* block_table,
-                                     int bt_stride, const void* kv_layer, long long block_stride,
-                                     float scale, void* out, int ld_o, cudaStream_t stream) {
+extern "C" int hy_attn_prefill_paged(const void* q, int ld_q, int n_rows, int n_seqs,
+                                     const int* qstart, const int* offset, const int* slots,
+                                     int max_q, int n_heads, int n_kv_heads, int head_dim,
+                                     const int* block_table, int bt_stride, const void* kv_layer,
+                                     long long block_stride, float scale, void* out, int ld_o,
+                                     cudaStream_t stream) {
   HY_CHECK_ARG(n_kv_heads > 0 && n_heads % n_kv_heads == 0, "heads");
-  if (n_seqs <= 0 || max_q <= 0) return 0;
+  if (n_seqs <= 0 || max_q <= 0 || n_rows <= 0) return 0;
+  if (use_tc(head_dim))
+    return attn_tc_prefill(q, ld_q, n_rows, n_seqs, qstart, offset, slots, max_q, n_heads,
+                           n_kv_heads, head_dim, block_table, bt_stride, kv_layer, block_stride,
+                           scale, out, ld_o, stream);
   FaParams p{};
   p.q = reinterpret_cast<const bf16*>(q);
   p.ld_q = ld_q;
@@ -300,10 +318,13 @@ extern "C" int hy_attn_prefill_paged(const void* q, int ld_q, int n_seqs, const 
   }
 }
 
-extern "C" int hy_attn_varlen(const void* qkv, int ld_qkv, int n_segs, const int* seg, int max_len,
-                              int n_heads, int head_dim, float scale, void* out, int ld_o,
-                              cudaStream_t stream) {
-  if (n_segs <= 0 || max_len <= 0) return 0;
+extern "C" int hy_attn_varlen(const void* qkv, int ld_qkv, int n_rows, int n_segs, const int* seg,
+                              int max_len, int n_heads, int head_dim, float scale, void* out,
+                              int ld_o, cudaStream_t stream) {
+  if (n_segs <= 0 || max_len <= 0 || n_rows <= 0) return 0;
+  if (use_tc(head_dim))
+    return attn_tc_varlen(qkv, ld_qkv, n_rows, n_segs, seg, max_len, n_heads, head_dim, scale,
+                          out, ld_o, stream);
   FaParams p{};
   const bf16* base = reinterpret_cast<const bf16*>(qkv);
   p.q = base;

@@ -136,7 +136,7 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
     }
     if (b->n_prefill > 0 && np_rows > 0) {
       timer_mark(HY_KCLASS_PREFILL_ATTN, st, true, 0.0);
-      HY_RET_IF(hy_attn_prefill_paged(w.qkv + (size_t)nd * qkv_cols, qkv_cols, b->n_prefill,
+      HY_RET_IF(hy_attn_prefill_paged(w.qkv + (size_t)nd * qkv_cols, qkv_cols, np_rows, b->n_prefill,
                                       b->pf_qstart, b->pf_offset, b->pf_slot, b->pf_max_q,
                                       m->n_heads, m->n_kv_heads, D, kv->block_table,
                                       kv->bt_stride, kv_layer, kv->block_stride, scale,
@@ -237,7 +237,7 @@ extern "C" int hy_vit_forward(const HyVitModel* m, const HyVitBatch* b, void* wo
     HY_RET_IF(G(w.t, Hv, L.w_qkv, T, 3 * Hv, Hv, L.b_qkv, nullptr, 0, HY_ACT_NONE, w.qkv, 3 * Hv,
                 nullptr));
     timer_mark(HY_KCLASS_VIT_ATTN, st, true, 0.0);
-    HY_RET_IF(hy_attn_varlen(w.qkv, 3 * Hv, b->n_images, b->seg, b->max_image_tokens, m->n_heads,
+    HY_RET_IF(hy_attn_varlen(w.qkv, 3 * Hv, T, b->n_images, b->seg, b->max_image_tokens, m->n_heads,
                              m->head_dim, scale, w.a, Hv, st));
     timer_mark(HY_KCLASS_VIT_ATTN, st, false, 0.0);
     HY_RET_IF(G(w.a, Hv, L.w_o, T, Hv, Hv, L.b_o, w.h, Hv, HY_ACT_NONE, w.h, Hv, nullptr));

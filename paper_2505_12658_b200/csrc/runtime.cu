@@ -12,10 +12,15 @@ static std::atomic<long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// Programmatic dependent launch is OFF by default (HY_PDL=1 enables it).  With PDL on, the
+// two-stream serving replay (vision stream at high priority, or the CTA-pair GEMM releasing
+// its dependents early) hung on B200 within minutes; with it off, no hang was seen in any
+// run.  The kernels keep their griddepcontrol points, which are no-ops without the launch
+// attribute.  Cost: the next kernel's prologue no longer overlaps the previous kernel's tail.
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("HY_PDL");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }

@@ -198,6 +198,7 @@ def test_decode_attention(n_heads, n_kv, ctxs):
     (4, 4, [(0, 70), (100, 37), (16, 64)]),           # (offset, chunk)
     (32, 32, [(0, 616)]),
     (28, 4, [(576, 40), (0, 129)]),
+    (8, 8, [(1000, 300), (0, 1), (127, 129)]),         # many KV tiles, 1-row chunk
 ])
 def test_prefill_attention_paged(n_heads, n_kv, chunks):
     d, L, layer = 128, 2, 0
@@ -205,12 +206,13 @@ def test_prefill_attention_paged(n_heads, n_kv, chunks):
     n = len(chunks)
     kv, bt, bts, be = _paged_setup(n, ctxs, n_kv, d, L, layer, seed=1)
     rows = sum(c for _, c in chunks)
-    q = torch.randn(rows, n_heads * d, device=DEV).bfloat16()
+    # scaled queries: the running row max jumps across KV tiles (online-softmax rescale path)
+    q = (torch.randn(rows, n_heads * d, device=DEV) * 3).bfloat16()
     out = torch.empty(rows, n_heads * d, device=DEV, dtype=torch.bfloat16)
     qstart = torch.tensor(np.cumsum([0] + [c for _, c in chunks]), dtype=torch.int32, device=DEV)
     offs = torch.tensor([o for o, _ in chunks], dtype=torch.int32, device=DEV)
     slots = torch.arange(n, dtype=torch.int32, device=DEV)
-    ck(lib().hy_attn_prefill_paged(q.data_ptr(), n_heads * d, n, qstart.data_ptr(),
+    ck(lib().hy_attn_prefill_paged(q.data_ptr(), n_heads * d, rows, n, qstart.data_ptr(),
                                    offs.data_ptr(), slots.data_ptr(), max(c for _, c in chunks),
                                    n_heads, n_kv, d, bt.data_ptr(), bts, kv.data_ptr(), be,
                                    1 / math.sqrt(d), out.data_ptr(), n_heads * d, st()), "prefill")
@@ -227,14 +229,15 @@ def test_prefill_attention_paged(n_heads, n_kv, chunks):
         r0 += c
 
 
-@pytest.mark.parametrize("d,lens", [(64, [577, 577, 10]), (80, [1024, 64, 300]), (128, [65])])
+@pytest.mark.parametrize("d,lens", [(64, [577, 577, 10]), (80, [1024, 64, 300]), (128, [65]),
+                                    (128, [300, 129, 1])])
 def test_vit_varlen_attention(d, lens):
     nh = 4
     T = sum(lens)
     qkv = torch.randn(T, 3 * nh * d, device=DEV).bfloat16()
     out = torch.empty(T, nh * d, device=DEV, dtype=torch.bfloat16)
     seg = torch.tensor(np.cumsum([0] + lens), dtype=torch.int32, device=DEV)
-    ck(lib().hy_attn_varlen(qkv.data_ptr(), 3 * nh * d, len(lens), seg.data_ptr(), max(lens),
+    ck(lib().hy_attn_varlen(qkv.data_ptr(), 3 * nh * d, sum(lens), len(lens), seg.data_ptr(), max(lens),
                             nh, d, 1 / math.sqrt(d), out.data_ptr(), nh * d, st()), "varlen")
     r0 = 0
     for n in lens:

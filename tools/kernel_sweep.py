@@ -145,7 +145,7 @@ def attn_sweep(out):
         seg = torch.arange(0, tot + 1, T, dtype=torch.int32, device=DEV)
 
         def ours(i):
-            rc = lib().hy_attn_varlen(qkv.data_ptr(), 3 * nh * d, n_img, seg.data_ptr(), T, nh, d,
+            rc = lib().hy_attn_varlen(qkv.data_ptr(), 3 * nh * d, tot, n_img, seg.data_ptr(), T, nh, d,
                                       1 / math.sqrt(d), o.data_ptr(), nh * d, st())
             assert rc == 0, lib().hy_last_error()
         t0 = timeit(ours)
@@ -189,7 +189,7 @@ def attn_sweep(out):
         mq = max(c for _, c in chunks)
 
         def ours(i):
-            rc = lib().hy_attn_prefill_paged(q.data_ptr(), nh * d, n, qstart.data_ptr(),
+            rc = lib().hy_attn_prefill_paged(q.data_ptr(), nh * d, rows, n, qstart.data_ptr(),
                                              offs.data_ptr(), slots.data_ptr(), mq, nh, nh, d,
                                              bt.data_ptr(), bts, kv.data_ptr(), block_elems,
                                              1 / math.sqrt(d), o.data_ptr(), nh * d, st())
