@@ -97,7 +97,8 @@ int hy_gemm_bf16(const void* A, int lda, const void* W, int ldw, int M, int N, i
                  const HyGemmEpilogue* epi, void* workspace, size_t workspace_bytes,
                  cudaStream_t stream);
 /* mode 0 = heuristic, 1 = force swap-AB (decode orientation), 2 = force normal (one CTA per
- * tile), 3 = force the CTA-pair kernel (cta_group::2, 256-row tiles; N % 256 == 0) */
+ * tile), 3 = force the CTA-pair kernel (cta_group::2, 256-row tiles; 256-wide weight tiles, or
+ * 128-wide when N % 256 != 0; N % 128 == 0) */
 int hy_gemm_bf16_mode(const void* A, int lda, const void* W, int ldw, int M, int N, int K,
                       const HyGemmEpilogue* epi, void* workspace, size_t workspace_bytes,
                       int mode, cudaStream_t stream);

@@ -52,6 +52,16 @@ __global__ void rope_kv_append_kernel(bf16* __restrict__ qkv, int ld_qkv, int ro
   if (r >= rows) return;
   const int p = pos[r];
   const int half = d / 2;
+  // the rotation angles depend on (position, frequency) only: one sincos per frequency per
+  // row, shared by every q and k head (inv_freq_i = theta^(-2i/d) in fp32, HF-style)
+  __shared__ float2 cs[128];  // d <= 256
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    const float inv = 1.0f / powf(theta, (float)(2 * i) / (float)d);
+    float sn, cn;
+    sincosf((float)p * inv, &sn, &cn);
+    cs[i] = make_float2(cn, sn);
+  }
+  __syncthreads();
   const int pairs_per_head = half / 2;  // each thread handles dims (i, i+1) and (i+half, i+half+1)
   bf16* row = qkv + (size_t)r * ld_qkv;
   const int blk = block_table[(size_t)row_slot[r] * bt_stride + p / HY_KV_BLOCK_TOKENS];
@@ -64,19 +74,14 @@ __global__ void rope_kv_append_kernel(bf16* __restrict__ qkv, int ld_qkv, int ro
     if (j < n_rot) {
       int h = j / pairs_per_head;
       int i = (j % pairs_per_head) * 2;
-      // inv_freq_i = theta^(-2i/d), fp32 like the HF reference implementation
-      float inv0 = 1.0f / powf(theta, (float)(2 * i) / (float)d);
-      float inv1 = 1.0f / powf(theta, (float)(2 * (i + 1)) / (float)d);
-      float s0, c0, s1, c1;
-      sincosf((float)p * inv0, &s0, &c0);
-      sincosf((float)p * inv1, &s1, &c1);
+      const float2 a0 = cs[i], a1 = cs[i + 1];
       bf16* x = row + (size_t)h * d;  // q heads then k heads are contiguous
       float2 lo = unpack_bf16x2(*reinterpret_cast<uint32_t*>(x + i));
       float2 hi = unpack_bf16x2(*reinterpret_cast<uint32_t*>(x + i + half));
-      float o_lo0 = lo.x * c0 - hi.x * s0;
-      float o_lo1 = lo.y * c1 - hi.y * s1;
-      float o_hi0 = hi.x * c0 + lo.x * s0;
-      float o_hi1 = hi.y * c1 + lo.y * s1;
+      float o_lo0 = lo.x * a0.x - hi.x * a0.y;
+      float o_lo1 = lo.y * a1.x - hi.y * a1.y;
+      float o_hi0 = hi.x * a0.x + lo.x * a0.y;
+      float o_hi1 = hi.y * a1.x + lo.y * a1.y;
       uint32_t plo = pack_bf16x2(o_lo0, o_lo1), phi = pack_bf16x2(o_hi0, o_hi1);
       if (h < n_heads) {
         *reinterpret_cast<uint32_t*>(x + i) = plo;
@@ -360,7 +365,7 @@ extern "C" int hy_rope_kv_append(void* qkv, int ld_qkv, int rows, int n_heads, i
                                  int head_dim, const int* pos, const int* row_slot,
                                  const int* block_table, int bt_stride, void* kv_layer,
                                  long long block_stride, float rope_theta, cudaStream_t stream) {
-  HY_CHECK_ARG(head_dim % 4 == 0 && ld_qkv % 2 == 0, "rope: head_dim % 4");
+  HY_CHECK_ARG(head_dim % 4 == 0 && head_dim <= 256 && ld_qkv % 2 == 0, "rope: head_dim % 4, <= 256");
   if (rows <= 0) return 0;
   HY_CUDA_RET(launch_pdl(rope_kv_append_kernel, dim3(rows), dim3(256), 0, stream, 
       reinterpret_cast<bf16*>(qkv), ld_qkv, rows, n_heads, n_kv_heads, head_dim, pos, row_slot,

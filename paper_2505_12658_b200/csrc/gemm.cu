@@ -731,14 +731,15 @@ static int launch_pair(const CUtensorMap& tA, const CUtensorMap& tB, const GemmA
   return 0;
 }
 
+template <int BN>
 static int launch_pair_epi(int epi, const CUtensorMap& tA, const CUtensorMap& tB,
                            const GemmArgs& a, int grid, cudaStream_t st) {
   switch (epi) {
-    case EPI_BF16: return launch_pair<256, EPI_BF16>(tA, tB, a, grid, st);
-    case EPI_QGELU: return launch_pair<256, EPI_QGELU>(tA, tB, a, grid, st);
-    case EPI_GELU: return launch_pair<256, EPI_GELU>(tA, tB, a, grid, st);
-    case EPI_SWIGLU: return launch_pair<256, EPI_SWIGLU>(tA, tB, a, grid, st);
-    case EPI_F32: return launch_pair<256, EPI_F32>(tA, tB, a, grid, st);
+    case EPI_BF16: return launch_pair<BN, EPI_BF16>(tA, tB, a, grid, st);
+    case EPI_QGELU: return launch_pair<BN, EPI_QGELU>(tA, tB, a, grid, st);
+    case EPI_GELU: return launch_pair<BN, EPI_GELU>(tA, tB, a, grid, st);
+    case EPI_SWIGLU: return launch_pair<BN, EPI_SWIGLU>(tA, tB, a, grid, st);
+    case EPI_F32: return launch_pair<BN, EPI_F32>(tA, tB, a, grid, st);
     default: return -1;
   }
 }
@@ -829,18 +830,27 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   // CTA-pair kernel: large token counts, weight rows a multiple of 256
   // when it needs no more full waves than the single-CTA kernel (a pair tile takes about as
   // long on two SMs as a 128-row tile on one, so waves decide)
+  // Estimated time in units of one 256x256 pair-tile wave: full waves x relative tile time
+  // (pair BN=128 tiles: half the work, ~10% less efficient; single-CTA 128x256 tiles: ~12%
+  // less efficient than a pair tile).  Picks the pair tile width with the best wave fill.
   bool pair = force_mode == 3;
+  int pair_bn = 256;
   if (force_mode == 0 && M >= kPairMinRows && N % 256 == 0 && !getenv("HY_GEMM_NOPAIR")) {
     const int sms = num_sms();
-    const int waves_pair = ceil_div(ceil_div(M, 256) * (N / 256), sms / 2);
-    const int waves_single = ceil_div(ceil_div(M, 128) * (N / 256), sms);
-    pair = waves_pair <= waves_single;
+    const double t256 = ceil_div(ceil_div(M, 256) * (N / 256), sms / 2);
+    const double t128 = 0.55 * ceil_div(ceil_div(M, 256) * (N / 128), sms / 2);
+    const double t1 = 1.12 * ceil_div(ceil_div(M, 128) * (N / 256), sms);
+    pair = std::min(t256, t128) <= t1;
+    pair_bn = t128 < t256 ? 128 : 256;
+  } else if (force_mode == 3 && N % 256 != 0) {
+    pair_bn = 128;
   }
+  if (const char* e = getenv("HY_PAIR_BN")) pair_bn = atoi(e);  // tuning only
   if (pair) {
+    HY_CHECK_ARG(N % pair_bn == 0, "pair kernel needs N % 128 == 0");
     a.np = ceil_div(M, 256);
-    a.nq = N / 256;
+    a.nq = N / pair_bn;
     a.nkb = ceil_div(K, 64);
-    HY_CHECK_ARG(N % 256 == 0, "pair kernel needs N % 256 == 0");
     const int grid = 2 * std::min(a.np * a.nq, num_sms() / 2);
     // The pair kernel does not release its dependents early: with an early trigger, a
     // PDL-launched pair GEMM plus early-launched dependents hung the serving replay on B200
@@ -849,8 +859,9 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     if (const char* d = getenv("HY_PAIR_DBG")) a.dbg = atoi(d);
     CUtensorMap tA, tB;
     HY_RET_IF(make_tmap_2d_bf16(&tA, A, M, K, (uint64_t)lda * 2, 128, 64));
-    HY_RET_IF(make_tmap_2d_bf16(&tB, W, N, K, (uint64_t)ldw * 2, 128, 64));
-    const int rc = launch_pair_epi(epi, tA, tB, a, grid, st);
+    HY_RET_IF(make_tmap_2d_bf16(&tB, W, N, K, (uint64_t)ldw * 2, pair_bn / 2, 64));
+    const int rc = pair_bn == 128 ? launch_pair_epi<128>(epi, tA, tB, a, grid, st)
+                                  : launch_pair_epi<256>(epi, tA, tB, a, grid, st);
     if (rc < 0) {
       set_last_error("gemm: no pair kernel for this epilogue");
       return (int)cudaErrorInvalidValue;

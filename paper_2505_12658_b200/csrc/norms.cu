@@ -4,30 +4,49 @@
 #include "common.cuh"
 #include "../../include/hydra_sm100.h"
 
+#include <algorithm>
+
 namespace hy {
 
-template <bool LAYER>
-__global__ void norm_kernel(const bf16* __restrict__ x, int ldx, const bf16* __restrict__ w,
-                            const bf16* __restrict__ b, bf16* __restrict__ out, int ldo, int rows,
-                            int cols, float eps, const int* __restrict__ row_idx) {
+// One CTA per row, up to 4 16-byte vectors per thread held in registers: a single HBM read of
+// the row with every load in flight at once (the former warp-per-row version re-read the row
+// and left an SM with a few latency-bound warps for a ~1k-row batch).
+template <bool LAYER, int V>
+__global__ void __launch_bounds__(512)
+    norm_kernel(const bf16* __restrict__ x, int ldx, const bf16* __restrict__ w,
+                const bf16* __restrict__ b, bf16* __restrict__ out, int ldo, int rows, int cols,
+                float eps, const int* __restrict__ row_idx) {
   pdl_trigger();
   pdl_wait();
-  const int warps = blockDim.x >> 5;
-  const int r = blockIdx.x * warps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
+  const int r = blockIdx.x;
   const int src = row_idx ? row_idx[r] : r;
   const bf16* xr = x + (size_t)src * ldx;
+  const int nvec = cols >> 3;
+  float f[V][8];
   float s1 = 0.f, s2 = 0.f;
-  for (int c = lane * 8; c < cols; c += 256) {
-    float f[8];
-    load_bf16x8(xr + c, f);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      s1 += f[j];
-      s2 += f[j] * f[j];
+  for (int k = 0; k < V; ++k) {
+    const int v = threadIdx.x + k * blockDim.x;
+    if (v < nvec) {
+      load_bf16x8(xr + v * 8, f[k]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s1 += f[k][j];
+        s2 += f[k][j] * f[k][j];
+      }
     }
   }
+  __shared__ float red[2][16];
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (lane == 0) {
+    red[0][warp] = s1;
+    red[1][warp] = s2;
+  }
+  __syncthreads();
+  s1 = lane < nw ? red[0][lane] : 0.f;
+  s2 = lane < nw ? red[1][lane] : 0.f;
   s1 = warp_sum(s1);
   s2 = warp_sum(s2);
   float mean = 0.f, rstd;
@@ -39,20 +58,23 @@ __global__ void norm_kernel(const bf16* __restrict__ x, int ldx, const bf16* __r
     rstd = rsqrtf(s2 / cols + eps);
   }
   bf16* o = out + (size_t)r * ldo;
-  for (int c = lane * 8; c < cols; c += 256) {
-    float f[8], g[8];
-    load_bf16x8(xr + c, f);
-    load_bf16x8(w + c, g);
-    if (LAYER) {
-      float bb[8];
-      load_bf16x8(b + c, bb);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) f[j] = (f[j] - mean) * rstd * g[j] + bb[j];
-    } else {
+  for (int k = 0; k < V; ++k) {
+    const int v = threadIdx.x + k * blockDim.x;
+    if (v < nvec) {
+      float g[8];
+      load_bf16x8(w + v * 8, g);
+      if (LAYER) {
+        float bb[8];
+        load_bf16x8(b + v * 8, bb);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) f[j] = f[j] * rstd * g[j];
+        for (int j = 0; j < 8; ++j) f[k][j] = (f[k][j] - mean) * rstd * g[j] + bb[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[k][j] = f[k][j] * rstd * g[j];
+      }
+      store_bf16x8(o + v * 8, f[k]);
     }
-    store_bf16x8(o + c, f);
   }
 }
 
@@ -60,13 +82,22 @@ template <bool LAYER>
 static int launch_norm(const void* x, int ldx, const void* w, const void* b, void* out, int ldo,
                        int rows, int cols, float eps, const int* row_idx, cudaStream_t st) {
   HY_CHECK_ARG(cols % 8 == 0 && ldx % 8 == 0 && ldo % 8 == 0, "norm: cols/ld must be % 8");
+  HY_CHECK_ARG(cols <= 8 * 512 * 4, "norm: cols <= 16384");
   if (rows <= 0) return 0;
-  const int threads = 256;
-  const int rows_per_block = threads / 32;
-  HY_CUDA_RET(launch_pdl(norm_kernel<LAYER>, dim3(ceil_div(rows, rows_per_block)), dim3(threads), 0, st, 
-      reinterpret_cast<const bf16*>(x), ldx, reinterpret_cast<const bf16*>(w),
-      reinterpret_cast<const bf16*>(b), reinterpret_cast<bf16*>(out), ldo, rows, cols, eps,
-      row_idx));
+  const int nvec = cols / 8;
+  // threads: a multiple of 32, <= 512, each thread <= 4 vectors
+  int threads = std::min(512, ((nvec + 1) / 2 + 31) / 32 * 32);
+  threads = std::max(threads, 32);
+  const int per = ceil_div(nvec, threads);
+  auto args = [&](auto kern) {
+    return launch_pdl(kern, dim3(rows), dim3(threads), 0, st, reinterpret_cast<const bf16*>(x),
+                      ldx, reinterpret_cast<const bf16*>(w), reinterpret_cast<const bf16*>(b),
+                      reinterpret_cast<bf16*>(out), ldo, rows, cols, eps, row_idx);
+  };
+  if (per <= 2)
+    HY_CUDA_RET(args(norm_kernel<LAYER, 2>));
+  else
+    HY_CUDA_RET(args(norm_kernel<LAYER, 4>));
   HY_LAUNCH_CHECK();
   return 0;
 }
