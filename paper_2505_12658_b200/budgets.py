@@ -37,7 +37,7 @@ def _largest_true(lo: int, hi: int, pred: Callable[[int], bool]) -> int:
 
 
 class _Prober:
-    def __init__(self, rt, shape, repeats: int = 2):
+    def __init__(self, rt, shape, repeats: int = 5):
         self.rt = rt
         self.shape = shape
         self.repeats = repeats

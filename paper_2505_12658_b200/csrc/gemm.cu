@@ -831,8 +831,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   // when it needs no more full waves than the single-CTA kernel (a pair tile takes about as
   // long on two SMs as a 128-row tile on one, so waves decide)
   // Estimated time in units of one 256x256 pair-tile wave: full waves x relative tile time
-  // (pair BN=128 tiles: half the work, ~10% less efficient; single-CTA 128x256 tiles: ~12%
-  // less efficient than a pair tile).  Picks the pair tile width with the best wave fill.
+  // (single-CTA 128x256 tiles: ~12% less efficient than a pair tile).
   bool pair = force_mode == 3;
   int pair_bn = 256;
   if (force_mode == 0 && M >= kPairMinRows && N % 256 == 0 && !getenv("HY_GEMM_NOPAIR")) {
@@ -840,8 +839,11 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     const double t256 = ceil_div(ceil_div(M, 256) * (N / 256), sms / 2);
     const double t128 = 0.55 * ceil_div(ceil_div(M, 256) * (N / 128), sms / 2);
     const double t1 = 1.12 * ceil_div(ceil_div(M, 128) * (N / 256), sms);
-    pair = std::min(t256, t128) <= t1;
-    pair_bn = t128 < t256 ? 128 : 256;
+    pair = t256 <= t1;
+    // 128-wide pair tiles fill waves better on paper (t128) but measured slower inside the
+    // serving sequence (tools/batch_bench.py: 2816-token prefill 42.2 vs 38.8 ms); they are
+    // kept for N % 256 != 0 and HY_PAIR_BN=128 experiments
+    (void)t128;
   } else if (force_mode == 3 && N % 256 != 0) {
     pair_bn = 128;
   }
