@@ -1,21 +1,20 @@
 // K7 paged prefill attention and K3 ViT varlen attention on 5th-generation tensor cores.
 //
-// One CTA = one (sequence, query head, 128-row query tile).  Warp-specialised:
-//   warp 0      TMA producer: the Q tile once, then K/V tiles of 128 keys into a 2-stage ring
-//               (paged: eight 16-token cache blocks per tile through the block table;
+// One CTA = one (sequence, query head, two 128-row query tiles).  Warp-specialised:
+//   warp 0      TMA producer: both Q tiles once, then K/V tiles of 128 keys into a 2-stage
+//               ring (paged: eight 16-token cache blocks per tile through the block table;
 //               varlen: the image's rows of the packed QKV buffer)
-//   warp 1      single-thread tcgen05.mma issuer:
-//                 S_j = Q K_j^T   (M=128 queries, N=128 keys, K=d; fp32 in TMEM, double-buffered)
-//                 O  += P_j V_j   (M=128, N=d, K=128 keys; P from shared memory, V as an
-//                                  MN-major operand straight from its TMA tile)
-//               issued as S_0, S_1, PV_0, S_2, PV_1, ... so Q K^T of the next tile runs
-//               while the softmax warps work on the current one
-//   warps 2..5  softmax: each thread owns one query row -- tcgen05.ld of its S row, mask,
-//               online max/sum in the exp2 domain, P as bf16 into shared memory with the
-//               128-byte swizzle the MMA descriptor expects.  The O accumulator stays in
-//               TMEM; it is rescaled (tcgen05.ld/st of the row) only when the running max
-//               grows by more than 2^8 -- P values stay <= 256, exact in the final O / l.
-//               Finally O / l -> bf16 -> global.
+//   warp 1      single-thread tcgen05.mma issuer, per query tile t and key tile j:
+//                 S_t = Q_t K_j^T  (M=128 queries, N=128 keys, K=d; fp32 in TMEM)
+//                 O_t += P_t V_j   (M=128, N=d, K=128 keys; P_t read from TMEM where the
+//                                   softmax wrote it over S_t, V as an MN-major operand
+//                                   straight from its TMA tile)
+//               ping-pong: the MMAs of one tile run while the other tile's softmax works
+//   warps 2..9  softmax, 4 warps per query tile, one query row per thread: tcgen05.ld of
+//               the S row, mask, online max/sum in the exp2 domain, P as bf16 pairs
+//               tcgen05.st back into TMEM.  O stays in TMEM; it is rescaled (tcgen05.ld/st)
+//               only when a row max grows by more than 2^8 -- P stays <= 256, exact in the
+//               final O / l.  Finally O / l -> bf16 -> global.
 //
 // Same math as the mma.sync kernel it replaces for d in {64, 128} (attn_prefill.cu keeps
 // that kernel for other head sizes, e.g. Qwen2-VL's d = 80 vision tower).
@@ -28,13 +27,35 @@
 
 namespace hy {
 
+#ifdef HY_ATRACE
+// lab-only timeline of CTA 0: [event][j] globaltimer stamps
+__device__ unsigned long long g_atrace[8][64];
+#define ATR(ev, j)                                                         \
+  do {                                                                     \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 64) {                  \
+      unsigned long long t_;                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));               \
+      g_atrace[ev][j] = t_;                                                \
+    }                                                                      \
+  } while (0)
+#else
+#define ATR(ev, j)
+#endif
+
+// 2^x on the SFU (ex2.approx.ftz: ~2 ulp, far below the bf16 rounding of P)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 struct TcAttnParams {
   const int* qstart;   // [n_seqs + 1] query rows of each sequence in the Q map
   const int* offset;   // paged: tokens cached before the chunk
   const int* slots;    // paged: block-table row of each sequence
   const int* block_table;
   int bt_stride;
-  int q_tiles;         // 128-row query tiles per sequence in the grid
+  int q_tiles;         // 256-row query-tile pairs per sequence in the grid
   int group;           // query heads per kv head
   int k_col0, v_col0;  // varlen: column of kv head 0's K / V in the packed QKV map
   long long rows_per_block;  // paged: KV-map rows per cache block (block_stride / d)
@@ -47,51 +68,51 @@ struct TcAttnParams {
 template <int D>
 struct TcAttnCfg {
   static constexpr int BQ = 128, BK = 128;
+  static constexpr int TILES = 2;                 // query tiles per CTA (ping-pong)
   static constexpr int NC = D / 64;               // 64-wide d chunks (one 128B swizzle row)
   static constexpr int CHUNK = 128 * 128;         // bytes of one [128 rows][64 bf16] chunk
-  static constexpr int Q_BYTES = NC * CHUNK;
-  static constexpr int KV_BYTES = NC * CHUNK;     // K (or V) of one tile
+  static constexpr int Q_BYTES = NC * CHUNK;      // one query tile
+  static constexpr int KV_BYTES = NC * CHUNK;     // K (or V) of one key tile
   static constexpr int STAGE_BYTES = 2 * KV_BYTES;
-  static constexpr int P_BYTES = 2 * CHUNK;       // [128 q][128 keys] bf16, 2 key chunks
-  static constexpr int SMEM = Q_BYTES + 2 * STAGE_BYTES + P_BYTES + 1024 + 256;
-  static constexpr uint32_t TM_S = 0;             // S buffers at columns 0 and 128
-  static constexpr uint32_t TM_O = 256;           // O at columns 256 .. 256 + D
+  static constexpr int SMEM = TILES * Q_BYTES + 2 * STAGE_BYTES + 1024 + 256;
+  // TMEM columns: tile t owns S_t (fp32, 128 cols) at t * 128, overwritten in place by P_t
+  // (bf16 pairs, first 64 cols), and O_t at 256 + t * 128
   static constexpr int TMEM_COLS = 512;
+  static constexpr int THREADS = 64 + TILES * 128;
 };
 
 template <int D, bool PAGED>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(64 + 2 * 128, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                    const TcAttnParams p) {
   using C = TcAttnCfg<D>;
   pdl_trigger();
   pdl_wait();  // Q (and for varlen K/V) are written by the previous kernel on the stream
   const int seq = blockIdx.x / p.q_tiles;
-  const int qt = blockIdx.x % p.q_tiles;
+  const int qp = blockIdx.x % p.q_tiles;  // pair of 128-row query tiles
   const int h = blockIdx.y;
   const int kvh = h / p.group;
   const int q0 = p.qstart[seq];
   const int nq = p.qstart[seq + 1] - q0;
-  if (qt * C::BQ >= nq) return;
+  const int qbase = qp * C::TILES * C::BQ;  // first query row of this CTA within the sequence
+  if (qbase >= nq) return;
   const int off = PAGED ? p.offset[seq] : 0;
   const int kv_len = off + nq;
-  const int kv_end = PAGED ? min(kv_len, off + qt * C::BQ + C::BQ) : kv_len;
+  const int kv_end = PAGED ? min(kv_len, off + qbase + C::TILES * C::BQ) : kv_len;
   const int n_kt = (kv_end + C::BK - 1) / C::BK;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sKV = smem + C::Q_BYTES;                 // stage s: K at s * STAGE, V at + KV_BYTES
-  uint8_t* sP = sKV + 2 * C::STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::P_BYTES);
+  uint8_t* sQ = smem;                               // tile t at t * Q_BYTES
+  uint8_t* sKV = smem + C::TILES * C::Q_BYTES;      // stage s: K at s * STAGE, V at + KV_BYTES
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + 2 * C::STAGE_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_free = bars + 7;    // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* p_free = bars + 10;
+  uint64_t* kv_full = bars + 1;   // [2 stages]
+  uint64_t* kv_empty = bars + 3;  // [2 stages]
+  uint64_t* s_full = bars + 5;    // [2 tiles]
+  uint64_t* p_full = bars + 7;    // [2 tiles]
+  uint64_t* o_done = bars + 9;    // [2 tiles]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
 
   const int warp = threadIdx.x >> 5;
@@ -104,10 +125,9 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_done[i], 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(p_free, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -117,26 +137,39 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
+    // ---------------- TMA producer (lane 0 issues; the warp fetches block-table entries) --
     if (lane == 0) {
-      // ---------------- TMA producer ----------------
-      mbar_expect_tx(q_full, C::Q_BYTES);
-      for (int c = 0; c < C::NC; ++c)
-        tma_load_2d(&tmQ, q_full, sQ + c * C::CHUNK, h * D + c * 64, q0 + qt * C::BQ, kEvictFirst);
-      const int* bt = PAGED ? p.block_table + (size_t)p.slots[seq] * p.bt_stride : nullptr;
-      const int last_blk = (kv_end - 1) / HY_KV_BLOCK_TOKENS;
-      for (int j = 0; j < n_kt; ++j) {
-        const int st = j & 1;
+      mbar_expect_tx(q_full, C::TILES * C::Q_BYTES);
+      for (int t = 0; t < C::TILES; ++t)
+        for (int c = 0; c < C::NC; ++c)
+          tma_load_2d(&tmQ, q_full, sQ + t * C::Q_BYTES + c * C::CHUNK, h * D + c * 64,
+                      q0 + qbase + t * C::BQ, kEvictFirst);
+    }
+    constexpr int BPT = C::BK / HY_KV_BLOCK_TOKENS;  // cache blocks per key tile (8)
+    const int* bt = PAGED ? p.block_table + (size_t)p.slots[seq] * p.bt_stride : nullptr;
+    const int last_blk = (kv_end - 1) / HY_KV_BLOCK_TOKENS;
+    // lane b < 8 holds the physical id of block b of the current tile; the next tile's ids
+    // are fetched before waiting for the stage (one load latency per tile, overlapped).
+    // Blocks past the end reload the last valid one (finite data under masked keys).
+    int ids = 0;
+    if (PAGED && lane < BPT) ids = bt[min(lane, last_blk)];
+    for (int j = 0; j < n_kt; ++j) {
+      const int st = j & 1;
+      int next = 0;
+      if (PAGED && lane < BPT && j + 1 < n_kt) next = bt[min((j + 1) * BPT + lane, last_blk)];
+      uint8_t* sK = sKV + st * C::STAGE_BYTES;
+      uint8_t* sV = sK + C::KV_BYTES;
+      if (lane == 0) {
         mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        ATR(0, j);
         mbar_expect_tx(&kv_full[st], C::STAGE_BYTES);
-        uint8_t* sK = sKV + st * C::STAGE_BYTES;
-        uint8_t* sV = sK + C::KV_BYTES;
-        if (PAGED) {
-          // 8 cache blocks of 16 tokens; blocks past the end reload the last valid one
-          // (finite data under masked keys: P = 0 there, and 0 * finite = 0)
-#pragma unroll 1
-          for (int b = 0; b < C::BK / HY_KV_BLOCK_TOKENS; ++b) {
-            const int blk = min(j * (C::BK / HY_KV_BLOCK_TOKENS) + b, last_blk);
-            const long long row = (long long)bt[blk] * p.rows_per_block + kvh * HY_KV_BLOCK_TOKENS;
+      }
+      if (PAGED) {
+#pragma unroll
+        for (int b = 0; b < BPT; ++b) {
+          const int id = __shfl_sync(0xffffffffu, ids, b);
+          if (lane == 0) {
+            const long long row = (long long)id * p.rows_per_block + kvh * HY_KV_BLOCK_TOKENS;
 #pragma unroll
             for (int c = 0; c < C::NC; ++c) {
               tma_load_2d(&tmKV, &kv_full[st], sK + c * C::CHUNK + b * 2048, c * 64, (int)row,
@@ -145,90 +178,118 @@ __global__ void __launch_bounds__(192, 1)
                           (int)(row + p.rows_per_kv), kEvictNormal);
             }
           }
-        } else {
+        }
+      } else if (lane == 0) {
 #pragma unroll
-          for (int c = 0; c < C::NC; ++c) {
-            tma_load_2d(&tmKV, &kv_full[st], sK + c * C::CHUNK, p.k_col0 + kvh * D + c * 64,
-                        q0 + j * C::BK, kEvictNormal);
-            tma_load_2d(&tmKV, &kv_full[st], sV + c * C::CHUNK, p.v_col0 + kvh * D + c * 64,
-                        q0 + j * C::BK, kEvictNormal);
-          }
+        for (int c = 0; c < C::NC; ++c) {
+          tma_load_2d(&tmKV, &kv_full[st], sK + c * C::CHUNK, p.k_col0 + kvh * D + c * 64,
+                      q0 + j * C::BK, kEvictNormal);
+          tma_load_2d(&tmKV, &kv_full[st], sV + c * C::CHUNK, p.v_col0 + kvh * D + c * 64,
+                      q0 + j * C::BK, kEvictNormal);
         }
       }
+      ids = next;
+      __syncwarp();
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
+      // per tile t the chain S_t(j) -> softmax_t(j) -> PV_t(j) -> S_t(j+1) is serial (P_t
+      // lives in S_t's columns); the two tiles interleave so one tile's MMAs run while the
+      // other tile's softmax works.  MMAs from this thread execute in issue order.
       constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128);
       constexpr uint32_t idesc_pv = idesc_bf16_f32(128, D) | (1u << 16);  // B (= V) MN-major
-      auto issue_pv = [&](int i) {
-        mbar_wait(p_full, i & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(sKV + (i & 1) * C::STAGE_BYTES + C::KV_BYTES);
-        const uint32_t p_addr = smem_u32(sP);
-#pragma unroll
-        for (int kk = 0; kk < C::BK / 16; ++kk)
-          umma_bf16(tmem + C::TM_O, smem_desc_k_sw128(p_addr + (kk >> 2) * C::CHUNK + (kk & 3) * 32),
-                    smem_desc_sw128(v_addr + kk * 2048, C::CHUNK, 1024), idesc_pv,
-                    (i > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(p_free);
-        umma_commit(&kv_empty[i & 1]);
-      };
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      const uint32_t q_addr = smem_u32(sQ);
-      for (int j = 0; j < n_kt; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
-        mbar_wait(&s_free[st], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(sKV + st * C::STAGE_BYTES);
+      auto issue_s = [&](int t, int j) {
+        const uint32_t q_addr = smem_u32(sQ + t * C::Q_BYTES);
+        const uint32_t k_addr = smem_u32(sKV + (j & 1) * C::STAGE_BYTES);
 #pragma unroll
         for (int c = 0; c < C::NC; ++c)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_bf16(tmem + C::TM_S + st * 128, smem_desc_k_sw128(q_addr + c * C::CHUNK + k * 32),
+            umma_bf16(tmem + t * 128, smem_desc_k_sw128(q_addr + c * C::CHUNK + k * 32),
                       smem_desc_k_sw128(k_addr + c * C::CHUNK + k * 32), idesc_qk,
                       (c | k) ? 1u : 0u);
-        umma_commit(&s_full[st]);
-        if (j >= 1) issue_pv(j - 1);
+        umma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {
+        mbar_wait(&p_full[t], j & 1);
+        ATR(2 + t, j);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sKV + (j & 1) * C::STAGE_BYTES + C::KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < C::BK / 16; ++kk)
+          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                       smem_desc_sw128(v_addr + kk * 2048, C::CHUNK, 1024), idesc_pv,
+                       (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&o_done[t]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&kv_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < n_kt; ++j) {
+        const bool more = j + 1 < n_kt;
+        if (more) {
+          mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+          ATR(1, j + 1);
+          tc_fence_after();
+        }
+        for (int t = 0; t < C::TILES; ++t) {
+          issue_pv(t, j);
+          if (more) issue_s(t, j + 1);
+        }
+        umma_commit(&kv_empty[j & 1]);  // K_j and V_j retired once these MMAs complete
       }
-      issue_pv(n_kt - 1);
     }
   } else {
-    // ---------------- softmax warps 2..5: one query row per thread ----------------
+    // ---------------- softmax: tile t = warps 2..5 / 6..9, one query row per thread -------
+    const int t = (warp - 2) >> 2;
     const int sub = warp & 3;
     const int row = sub * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
-    const int qpos = off + qt * C::BQ + row;  // absolute position of this query
+    const uint32_t tl = tmem + ((uint32_t)(sub * 32) << 16);  // this warp's TMEM lanes
+    const uint32_t tS = tl + t * 128, tO = tl + 256 + t * 128;
+    const int qrow = qbase + t * C::BQ + row;  // query row within the sequence
+    const int qpos = off + qrow;               // absolute position of this query
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kt; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+      mbar_wait(&s_full[t], j & 1);
+      if (threadIdx.x == 64) ATR(4, j);
       tc_fence_after();
-      uint32_t r[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(trow + C::TM_S + b * 128 + c * 32, r + c * 32);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[b]);
+      // two passes over the S row in TMEM (re-reading is cheap; keeps ~64 live values so
+      // ten warps fit the per-scheduler register file): pass 1 row max, pass 2 P.  Tiles
+      // entirely inside every row's key range of the warp skip the per-element mask.
       const int kbase = j * C::BK;
-      float mx = -INFINITY;
+      const int kmax = PAGED ? min(kv_len, qpos + 1) : kv_len;  // keys [0, kmax) are valid
+      const bool full = __all_sync(0xffffffffu, kbase + C::BK <= kmax);
+      float mx8[8];
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        const int key = kbase + c;
-        const bool ok = key < kv_len && (!PAGED || key <= qpos);
-        const float x = ok ? __uint_as_float(r[c]) * p.scale_log2 : -INFINITY;
-        r[c] = __float_as_uint(x);
-        mx = fmaxf(mx, x);
+      for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; c += 2) {
+        uint32_t r[64];
+        tmem_ld_32x32b_x32(tS + c * 32, r);
+        tmem_ld_32x32b_x32(tS + c * 32 + 32, r + 32);
+        tmem_ld_wait();
+        if (full) {
+#pragma unroll
+          for (int u = 0; u < 64; ++u) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
+        } else {
+#pragma unroll
+          for (int u = 0; u < 64; ++u)
+            if (kbase + c * 32 + u < kmax) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
+        }
       }
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      mx = mx == -INFINITY ? mx : mx * p.scale_log2;
       const float m_new = fmaxf(m_used, mx);
       if (j >= 1) {
-        mbar_wait(p_free, (j - 1) & 1);  // PV_{j-1} retired: O stable, P buffer free
+        mbar_wait(&o_done[t], (j - 1) & 1);  // PV_t(j-1) retired: O_t stable
+        if (threadIdx.x == 64) ATR(6, j);
         tc_fence_after();
         // tcgen05.ld/st are warp-collective: the warp rescales together when any of its
-        // rows needs it (factor 1 for the others)
+        // rows' max grew by more than 2^8 (factor 1 for the others)
         const bool need = m_new > m_used + 8.f;
         if (__any_sync(0xffffffffu, need)) {
           const float f = !need ? 1.f : (m_used == -INFINITY ? 0.f : exp2f(m_used - m_new));
@@ -237,61 +298,67 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             uint32_t o[32];
-            tmem_ld_32x32b_x32(trow + C::TM_O + c * 32, o);
+            tmem_ld_32x32b_x32(tO + c * 32, o);
             tmem_ld_wait();
 #pragma unroll
-            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * f);
-            tmem_st_32x32b_x32(trow + C::TM_O + c * 32, o);
+            for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * f);
+            tmem_st_32x32b_x32(tO + c * 32, o);
           }
-          tmem_st_wait();
         }
       } else {
         m_used = m_new;
       }
       const float ms = m_used == -INFINITY ? 0.f : m_used;
-      // P row -> bf16, 128B-swizzled K-major tile: row `row`, 16-byte chunk c16 of key chunk kc
-      const uint32_t prow = smem_u32(sP) + (row >> 3) * 1024 + (row & 7) * 128;
-      float rs = 0.f;
+      // P_t = exp2(S * scale - m) as bf16 pairs into S_t's first 64 columns (A of PV); the
+      // P columns [32c, 32c+32) overwrite S columns that pass c already holds in registers
+      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+      const float sc = p.scale_log2;
 #pragma unroll
-      for (int kc = 0; kc < 2; ++kc)
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[64];
+        tmem_ld_32x32b_x32(tS + c * 64, r);
+        tmem_ld_32x32b_x32(tS + c * 64 + 32, r + 32);
+        tmem_ld_wait();
+        uint32_t pk[32];
 #pragma unroll
-        for (int c16 = 0; c16 < 8; ++c16) {
-          float e[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            e[t] = exp2f(__uint_as_float(r[kc * 64 + c16 * 8 + t]) - ms);
-            rs += e[t];
+        for (int u = 0; u < 32; ++u) {
+          float e0 = ex2_approx(fmaf(__uint_as_float(r[2 * u]), sc, -ms));
+          float e1 = ex2_approx(fmaf(__uint_as_float(r[2 * u + 1]), sc, -ms));
+          if (!full) {
+            const int key = kbase + c * 64 + 2 * u;
+            e0 = key < kmax ? e0 : 0.f;
+            e1 = key + 1 < kmax ? e1 : 0.f;
           }
-          const uint32_t a = prow + kc * C::CHUNK + ((c16 ^ (row & 7)) << 4);
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a),
-                       "r"(pack_bf16x2(e[0], e[1])), "r"(pack_bf16x2(e[2], e[3])),
-                       "r"(pack_bf16x2(e[4], e[5])), "r"(pack_bf16x2(e[6], e[7]))
-                       : "memory");
+          rs4[u & 3] += e0 + e1;
+          pk[u] = pack_bf16x2(e0, e1);
         }
+        tmem_st_32x32b_x32(tS + c * 32, pk);
+      }
+      const float rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
       l += rs;
-      fence_proxy_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[t]);
+      if (threadIdx.x == 64) ATR(5, j);
     }
-    // O / l -> global
-    mbar_wait(p_free, (n_kt - 1) & 1);
+    // O_t / l -> global
+    mbar_wait(&o_done[t], (n_kt - 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    const int qi = qt * C::BQ + row;
 #pragma unroll 1
     for (int c = 0; c < D / 32; ++c) {
       uint32_t o[32];
-      tmem_ld_32x32b_x32(trow + C::TM_O + c * 32, o);
+      tmem_ld_32x32b_x32(tO + c * 32, o);
       tmem_ld_wait();
-      if (qi < nq) {
-        bf16* dst = p.out + (size_t)(q0 + qi) * p.ld_o + (size_t)h * D + c * 32;
+      if (qrow < nq) {
+        bf16* dst = p.out + (size_t)(q0 + qrow) * p.ld_o + (size_t)h * D + c * 32;
 #pragma unroll
-        for (int t = 0; t < 32; t += 8) {
+        for (int u = 0; u < 32; u += 8) {
           float v[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = __uint_as_float(o[t + u]) * inv;
-          store_bf16x8(dst + t, v);
+          for (int w = 0; w < 8; ++w) v[w] = __uint_as_float(o[u + w]) * inv;
+          store_bf16x8(dst + u, v);
         }
       }
     }
@@ -314,8 +381,8 @@ static int launch_tc_attn(const CUtensorMap& tq, const CUtensorMap& tkv, const T
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  HY_CUDA_RET(launch_pdl(attn_tc_kernel<D, PAGED>, dim3(n_seqs * p.q_tiles, n_heads), dim3(192),
-                         C::SMEM, st, tq, tkv, p));
+  HY_CUDA_RET(launch_pdl(attn_tc_kernel<D, PAGED>, dim3(n_seqs * p.q_tiles, n_heads),
+                         dim3(C::THREADS), C::SMEM, st, tq, tkv, p));
   HY_LAUNCH_CHECK();
   return 0;
 }
@@ -334,7 +401,7 @@ int attn_tc_prefill(const void* q, int ld_q, int n_rows, int n_seqs, const int* 
   p.slots = slots;
   p.block_table = block_table;
   p.bt_stride = bt_stride;
-  p.q_tiles = ceil_div(max_q, 128);
+  p.q_tiles = ceil_div(max_q, 256);  // pairs of 128-row query tiles
   p.group = n_heads / n_kv_heads;
   p.rows_per_block = block_stride / head_dim;
   p.rows_per_kv = n_kv_heads * HY_KV_BLOCK_TOKENS;
@@ -358,7 +425,7 @@ int attn_tc_varlen(const void* qkv, int ld_qkv, int n_rows, int n_segs, const in
   HY_CHECK_ARG(head_dim == 128 || head_dim == 64, "tcgen05 attention: head_dim 64 or 128");
   TcAttnParams p{};
   p.qstart = seg;
-  p.q_tiles = ceil_div(max_len, 128);
+  p.q_tiles = ceil_div(max_len, 256);
   p.group = 1;
   p.k_col0 = n_heads * head_dim;
   p.v_col0 = 2 * n_heads * head_dim;

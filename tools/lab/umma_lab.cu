@@ -76,6 +76,67 @@ __global__ void __launch_bounds__(128, 1) k(const __grid_constant__ CUtensorMap 
   if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 128); }
 }
 
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                        uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// P from TMEM: columns 128..159 hold P[row][2j], P[row][2j+1] packed bf16x2
+__global__ void __launch_bounds__(128, 1) k_ts(const __grid_constant__ CUtensorMap tmV, const bf16* P,
+                                               float* D, int pack_swap) {
+  extern __shared__ __align__(1024) uint8_t sraw[];
+  uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sraw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sV = s;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s + 16384);
+  uint64_t* mbar = bar + 1;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) { mbar_init(bar, 1); mbar_init(mbar, 1); fence_mbar_init(); }
+  if (warp == 0) tmem_alloc(slot, 256);
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const uint32_t tmem = *slot;
+  if (tid == 0) {
+    mbar_expect_tx(bar, 16384);
+    tma_load_2d(&tmV, bar, sV, 0, 0, kEvictNormal);
+    tma_load_2d(&tmV, bar, sV + 8192, 64, 0, kEvictNormal);
+  }
+  {
+    uint32_t r[32];
+    for (int j = 0; j < 32; ++j) {
+      float a = __bfloat162float(P[tid * 64 + 2 * j]), b = __bfloat162float(P[tid * 64 + 2 * j + 1]);
+      r[j] = pack_swap ? pack_bf16x2(b, a) : pack_bf16x2(a, b);
+    }
+    tmem_st_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + 128, r);
+    tmem_st_wait();
+  }
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  if (tid == 0) {
+    mbar_wait(bar, 0);
+    tc_fence_after();
+    const uint32_t idesc = idesc_bf16_f32(128, 128) | (1u << 16);
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint64_t b = smem_desc_sw128(smem_u32(sV) + kk * 2048, 8192, 1024);
+      umma_ts(tmem, tmem + 128 + kk * 8, b, idesc, kk > 0 ? 1u : 0u);
+    }
+    umma_commit(mbar);
+  }
+  mbar_wait(mbar, 0);
+  tc_fence_after();
+  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  for (int c = 0; c < 4; ++c) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(taddr + c * 32, r);
+    tmem_ld_wait();
+    for (int j = 0; j < 32; ++j) D[tid * 128 + c * 32 + j] = __uint_as_float(r[j]);
+  }
+  tc_fence_before(); __syncthreads();
+  if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 256); }
+}
+
 int main() {
   std::vector<uint16_t> hP(128 * 64), hV(64 * 128);
   std::vector<float> fP(128 * 64), fV(64 * 128);
@@ -108,6 +169,18 @@ int main() {
     double err = 0;
     for (int i = 0; i < 128 * 128; ++i) err = fmax(err, fabs(hD[i] - ref[i]));
     printf("LBO %5u SBO %5u: max err %.4g %s\n", v[0], v[1], err, e ? cudaGetErrorString(e) : "");
+    if (e) return 1;
+  }
+  cudaFuncSetAttribute(k_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, 40 * 1024);
+  for (int sw = 0; sw < 2; ++sw) {
+    cudaMemset(dD, 0, 128 * 128 * 4);
+    k_ts<<<1, 128, 40 * 1024>>>(tm, dP, dD, sw);
+    cudaError_t e = cudaDeviceSynchronize();
+    std::vector<float> hD(128 * 128);
+    cudaMemcpy(hD.data(), dD, hD.size() * 4, cudaMemcpyDeviceToHost);
+    double err = 0;
+    for (int i = 0; i < 128 * 128; ++i) err = fmax(err, fabs(hD[i] - ref[i]));
+    printf("A from TMEM, pack_swap %d: max err %.4g %s\n", sw, err, e ? cudaGetErrorString(e) : "");
     if (e) return 1;
   }
   return 0;
