@@ -89,7 +89,9 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
   pdl_trigger();
   pdl_wait();  // Q (and for varlen K/V) are written by the previous kernel on the stream
   const int seq = blockIdx.x / p.q_tiles;
-  const int qp = blockIdx.x % p.q_tiles;  // pair of 128-row query tiles
+  // pair of 128-row query tiles, last pair first: under the causal mask later pairs see more
+  // keys, so the heavy CTAs start in the first wave and the light ones fill the tail
+  const int qp = p.q_tiles - 1 - blockIdx.x % p.q_tiles;
   const int h = blockIdx.y;
   const int kvh = h / p.group;
   const int q0 = p.qstart[seq];
