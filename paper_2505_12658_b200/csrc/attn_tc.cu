@@ -190,6 +190,22 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
                       q0 + j * C::BK, kEvictNormal);
         }
       }
+      // warm L2 with the next tile's blocks: its TMA loads (issued once a stage frees up)
+      // then hit L2 instead of HBM -- the 32 small boxes per tile are latency-bound
+      if (PAGED && j + 1 < n_kt) {
+#pragma unroll
+        for (int b = 0; b < BPT; ++b) {
+          const int id = __shfl_sync(0xffffffffu, next, b);
+          if (lane == 0) {
+            const long long row = (long long)id * p.rows_per_block + kvh * HY_KV_BLOCK_TOKENS;
+#pragma unroll
+            for (int c = 0; c < C::NC; ++c) {
+              tma_prefetch_2d(&tmKV, c * 64, (int)row);
+              tma_prefetch_2d(&tmKV, c * 64, (int)(row + p.rows_per_kv));
+            }
+          }
+        }
+      }
       ids = next;
       __syncwarp();
     }
@@ -232,14 +248,16 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
       issue_s(1, 0);
       for (int j = 0; j < n_kt; ++j) {
         const bool more = j + 1 < n_kt;
-        if (more) {
-          mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-          ATR(1, j + 1);
-          tc_fence_after();
-        }
         for (int t = 0; t < C::TILES; ++t) {
           issue_pv(t, j);
-          if (more) issue_s(t, j + 1);
+          if (more) {
+            if (t == 0) {  // the next key tile is needed only from here on
+              mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+              ATR(1, j + 1);
+              tc_fence_after();
+            }
+            issue_s(t, j + 1);
+          }
         }
         umma_commit(&kv_empty[j & 1]);  // K_j and V_j retired once these MMAs complete
       }
@@ -258,29 +276,26 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
       mbar_wait(&s_full[t], j & 1);
       if (threadIdx.x == 64) ATR(4, j);
       tc_fence_after();
-      // two passes over the S row in TMEM (re-reading is cheap; keeps ~64 live values so
-      // ten warps fit the per-scheduler register file): pass 1 row max, pass 2 P.  Tiles
-      // entirely inside every row's key range of the warp skip the per-element mask.
+      // one TMEM round trip for the whole S row (4 loads, one wait); the row stays in
+      // registers for the P pass.  Tiles entirely inside every row's key range of the warp
+      // skip the per-element mask.
       const int kbase = j * C::BK;
       const int kmax = PAGED ? min(kv_len, qpos + 1) : kv_len;  // keys [0, kmax) are valid
       const bool full = __all_sync(0xffffffffu, kbase + C::BK <= kmax);
+      uint32_t r[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tS + c * 32, r + c * 32);
+      tmem_ld_wait();
       float mx8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+      if (full) {
 #pragma unroll
-      for (int c = 0; c < 4; c += 2) {
-        uint32_t r[64];
-        tmem_ld_32x32b_x32(tS + c * 32, r);
-        tmem_ld_32x32b_x32(tS + c * 32 + 32, r + 32);
-        tmem_ld_wait();
-        if (full) {
+        for (int u = 0; u < 128; ++u) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
+      } else {
 #pragma unroll
-          for (int u = 0; u < 64; ++u) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
-        } else {
-#pragma unroll
-          for (int u = 0; u < 64; ++u)
-            if (kbase + c * 32 + u < kmax) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
-        }
+        for (int u = 0; u < 128; ++u)
+          if (kbase + u < kmax) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
       }
       float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
@@ -311,30 +326,26 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
         m_used = m_new;
       }
       const float ms = m_used == -INFINITY ? 0.f : m_used;
-      // P_t = exp2(S * scale - m) as bf16 pairs into S_t's first 64 columns (A of PV); the
-      // P columns [32c, 32c+32) overwrite S columns that pass c already holds in registers
+      // P_t = exp2(S * scale - m) as bf16 pairs into S_t's first 64 columns (A of PV), 16
+      // columns per store; column c of P holds keys 2c, 2c+1 (already in registers)
       float rs4[4] = {0.f, 0.f, 0.f, 0.f};
       const float sc = p.scale_log2;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t r[64];
-        tmem_ld_32x32b_x32(tS + c * 64, r);
-        tmem_ld_32x32b_x32(tS + c * 64 + 32, r + 32);
-        tmem_ld_wait();
-        uint32_t pk[32];
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          float e0 = ex2_approx(fmaf(__uint_as_float(r[2 * u]), sc, -ms));
-          float e1 = ex2_approx(fmaf(__uint_as_float(r[2 * u + 1]), sc, -ms));
+        for (int u = 0; u < 16; ++u) {
+          const int k0 = c * 32 + 2 * u;
+          float e0 = ex2_approx(fmaf(__uint_as_float(r[k0]), sc, -ms));
+          float e1 = ex2_approx(fmaf(__uint_as_float(r[k0 + 1]), sc, -ms));
           if (!full) {
-            const int key = kbase + c * 64 + 2 * u;
-            e0 = key < kmax ? e0 : 0.f;
-            e1 = key + 1 < kmax ? e1 : 0.f;
+            e0 = kbase + k0 < kmax ? e0 : 0.f;
+            e1 = kbase + k0 + 1 < kmax ? e1 : 0.f;
           }
           rs4[u & 3] += e0 + e1;
           pk[u] = pack_bf16x2(e0, e1);
         }
-        tmem_st_32x32b_x32(tS + c * 32, pk);
+        tmem_st_32x32b_x16(tS + c * 16, pk);
       }
       const float rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
       l += rs;
