@@ -62,12 +62,45 @@ __global__ void rope_kv_append_kernel(bf16* __restrict__ qkv, int ld_qkv, int ro
     cs[i] = make_float2(cn, sn);
   }
   __syncthreads();
-  const int pairs_per_head = half / 2;  // each thread handles dims (i, i+1) and (i+half, i+half+1)
   bf16* row = qkv + (size_t)r * ld_qkv;
   const int blk = block_table[(size_t)row_slot[r] * bt_stride + p / HY_KV_BLOCK_TOKENS];
   const int tk = p % HY_KV_BLOCK_TOKENS;
   bf16* kbase = kv + (size_t)blk * block_stride;
   bf16* vbase = kbase + (size_t)n_kv * HY_KV_BLOCK_TOKENS * d;
+  if ((half & 7) == 0 && (ld_qkv & 7) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0) {
+    // 16-byte vectors: a work item is 8 dims [i, i+8) of the first half and the matching
+    // 8 of the second half of one q/k head, or 8 dims of one v head
+    const int vph = half / 8;  // vector pairs per head
+    const int n_rot = (n_heads + n_kv) * vph;
+    const int total = n_rot + n_kv * (d / 8);
+    for (int j = threadIdx.x; j < total; j += blockDim.x) {
+      if (j < n_rot) {
+        const int h = j / vph;
+        const int i = (j % vph) * 8;
+        bf16* x = row + (size_t)h * d;
+        float lo[8], hi[8], olo[8], ohi[8];
+        load_bf16x8(x + i, lo);
+        load_bf16x8(x + i + half, hi);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const float2 a = cs[i + t];
+          olo[t] = lo[t] * a.x - hi[t] * a.y;
+          ohi[t] = hi[t] * a.x + lo[t] * a.y;
+        }
+        bf16* dst = h < n_heads ? x : kbase + ((size_t)(h - n_heads) * HY_KV_BLOCK_TOKENS + tk) * d;
+        store_bf16x8(dst + i, olo);
+        store_bf16x8(dst + i + half, ohi);
+      } else {
+        const int jj = j - n_rot;
+        const int vh = jj / (d / 8);
+        const int i = (jj % (d / 8)) * 8;
+        const uint4 v = *reinterpret_cast<const uint4*>(row + (size_t)(n_heads + n_kv + vh) * d + i);
+        *reinterpret_cast<uint4*>(vbase + ((size_t)vh * HY_KV_BLOCK_TOKENS + tk) * d + i) = v;
+      }
+    }
+    return;
+  }
+  const int pairs_per_head = half / 2;  // each thread handles dims (i, i+1) and (i+half, i+half+1)
   const int n_rot = (n_heads + n_kv) * pairs_per_head;
   const int total = n_rot + n_kv * (d / 2);
   for (int j = threadIdx.x; j < total; j += blockDim.x) {

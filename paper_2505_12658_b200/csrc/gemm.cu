@@ -787,6 +787,16 @@ static int launch_epi(int epi, int bn, const CUtensorMap& tA, const CUtensorMap&
 // Workspace layout: [counters: 16 KiB][partials: G * 2 * 128 * BN fp32].  The counter
 // region must be zero before first use; every call leaves it zeroed again.
 static constexpr size_t kCounterBytes = 16384;
+
+// SMs a GEMM grid may occupy (HY_GEMM_SMS caps it, e.g. to leave SMs to a concurrent stream)
+static int gemm_sms() {
+  static const int cap = [] {
+    const char* e = getenv("HY_GEMM_SMS");
+    return e ? atoi(e) : 0;
+  }();
+  const int n = num_sms();
+  return cap > 0 && cap < n ? cap : n;
+}
 // token rows from which the CTA-pair kernel is used (tuned on B200, tools/kernel_sweep.py)
 static constexpr int kPairMinRows = 512;
 
@@ -835,7 +845,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   bool pair = force_mode == 3;
   int pair_bn = 256;
   if (force_mode == 0 && M >= kPairMinRows && N % 256 == 0 && !getenv("HY_GEMM_NOPAIR")) {
-    const int sms = num_sms();
+    const int sms = gemm_sms();
     const double t256 = ceil_div(ceil_div(M, 256) * (N / 256), sms / 2);
     const double t128 = 0.55 * ceil_div(ceil_div(M, 256) * (N / 128), sms / 2);
     const double t1 = 1.12 * ceil_div(ceil_div(M, 128) * (N / 256), sms);
@@ -853,7 +863,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     a.np = ceil_div(M, 256);
     a.nq = N / pair_bn;
     a.nkb = ceil_div(K, 64);
-    const int grid = 2 * std::min(a.np * a.nq, num_sms() / 2);
+    const int grid = 2 * std::min(a.np * a.nq, gemm_sms() / 2);
     // The pair kernel does not release its dependents early: with an early trigger, a
     // PDL-launched pair GEMM plus early-launched dependents hung the serving replay on B200
     // (bisected with HY_PAIR_DBG: trigger off or PDL launch off both run clean).
@@ -887,7 +897,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   a.nq = ceil_div(a.Q, bn);
   a.nkb = ceil_div(K, 64);
   const int T = a.np * a.nq;
-  const int sms = num_sms();
+  const int sms = gemm_sms();
   const size_t need = kCounterBytes + (size_t)sms * 2 * 128 * bn * sizeof(float);
   // stream-K only when whole-tile waves would leave the machine badly underfilled
   const double dp_eff = (double)T / ((double)ceil_div(T, sms) * sms);
