@@ -221,9 +221,11 @@ struct GemmCfg {
   static constexpr int THREADS = 64 + 32 * kEpiWarps;
 };
 
-// raster index -> (p, q): groups of 8 p-tiles sweep all q-tiles (L2 reuse)
+// raster index -> (p, q): groups of p-tiles sweep all q-tiles (L2 reuse): with up to 16
+// p-tiles (token tiles) one group holds all of them, so each weight tile is streamed from HBM
+// once while the activations stay in L2; larger M uses groups of 8
 __device__ __forceinline__ void raster_tile(int t, const GemmArgs& a, int& p, int& q) {
-  constexpr int G8 = 8;
+  const int G8 = a.np <= 16 ? a.np : 8;
   const int span = G8 * a.nq;
   const int g = t / span;
   const int first_p = g * G8;
