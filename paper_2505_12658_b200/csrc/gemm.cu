@@ -59,6 +59,7 @@ struct GemmArgs {
   int np, nq, nkb;
   int t_dp;       // whole tiles [0, t_dp) round-robin (multiple of the grid when stream-K)
   int dbg;        // pair kernel PDL bits (HY_PAIR_DBG): 1 no early trigger, 2 no PDL launch
+  int group;      // raster group of token tiles (0 = auto; HY_GEMM_GROUP tuning only)
   long long u_sk; // k-block units of tiles [t_dp, T), split evenly over the grid
   int M, N;       // logical GEMM shape (tokens, physical weight rows)
   const bf16* bias;
@@ -225,7 +226,7 @@ struct GemmCfg {
 // p-tiles (token tiles) one group holds all of them, so each weight tile is streamed from HBM
 // once while the activations stay in L2; larger M uses groups of 8
 __device__ __forceinline__ void raster_tile(int t, const GemmArgs& a, int& p, int& q) {
-  const int G8 = a.np <= 16 ? a.np : 8;
+  const int G8 = a.group > 0 ? min(a.group, a.np) : (a.np <= 16 ? a.np : 8);
   const int span = G8 * a.nq;
   const int g = t / span;
   const int first_p = g * G8;
@@ -871,6 +872,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     // (bisected with HY_PAIR_DBG: trigger off or PDL launch off both run clean).
     a.dbg = 1;
     if (const char* d = getenv("HY_PAIR_DBG")) a.dbg = atoi(d);
+    if (const char* g = getenv("HY_GEMM_GROUP")) a.group = atoi(g);
     CUtensorMap tA, tB;
     HY_RET_IF(make_tmap_2d_bf16(&tA, A, M, K, (uint64_t)lda * 2, 128, 64));
     HY_RET_IF(make_tmap_2d_bf16(&tB, W, N, K, (uint64_t)ldw * 2, pair_bn / 2, 64));
@@ -895,6 +897,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     a.Q = N;
   }
   if (const char* env_bn = getenv("HY_GEMM_BN")) bn = atoi(env_bn);  // tuning only
+  if (const char* g = getenv("HY_GEMM_GROUP")) a.group = atoi(g);
   a.np = ceil_div(a.P, 128);
   a.nq = ceil_div(a.Q, bn);
   a.nkb = ceil_div(K, 64);
