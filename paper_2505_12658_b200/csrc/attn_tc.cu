@@ -166,19 +166,17 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
         ATR(0, j);
         mbar_expect_tx(&kv_full[st], C::STAGE_BYTES);
       }
+      __syncwarp();  // expect_tx (lane 0) precedes every lane's loads on this barrier
       if (PAGED) {
+        // lane b issues block b's boxes: eight lanes drive the TMA unit in parallel
+        if (lane < BPT) {
+          const long long row = (long long)ids * p.rows_per_block + kvh * HY_KV_BLOCK_TOKENS;
 #pragma unroll
-        for (int b = 0; b < BPT; ++b) {
-          const int id = __shfl_sync(0xffffffffu, ids, b);
-          if (lane == 0) {
-            const long long row = (long long)id * p.rows_per_block + kvh * HY_KV_BLOCK_TOKENS;
-#pragma unroll
-            for (int c = 0; c < C::NC; ++c) {
-              tma_load_2d(&tmKV, &kv_full[st], sK + c * C::CHUNK + b * 2048, c * 64, (int)row,
-                          kEvictNormal);
-              tma_load_2d(&tmKV, &kv_full[st], sV + c * C::CHUNK + b * 2048, c * 64,
-                          (int)(row + p.rows_per_kv), kEvictNormal);
-            }
+          for (int c = 0; c < C::NC; ++c) {
+            tma_load_2d(&tmKV, &kv_full[st], sK + c * C::CHUNK + lane * 2048, c * 64, (int)row,
+                        kEvictNormal);
+            tma_load_2d(&tmKV, &kv_full[st], sV + c * C::CHUNK + lane * 2048, c * 64,
+                        (int)(row + p.rows_per_kv), kEvictNormal);
           }
         }
       } else if (lane == 0) {
@@ -192,18 +190,12 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
       }
       // warm L2 with the next tile's blocks: its TMA loads (issued once a stage frees up)
       // then hit L2 instead of HBM -- the 32 small boxes per tile are latency-bound
-      if (PAGED && j + 1 < n_kt) {
+      if (PAGED && j + 1 < n_kt && lane < BPT) {
+        const long long row = (long long)next * p.rows_per_block + kvh * HY_KV_BLOCK_TOKENS;
 #pragma unroll
-        for (int b = 0; b < BPT; ++b) {
-          const int id = __shfl_sync(0xffffffffu, next, b);
-          if (lane == 0) {
-            const long long row = (long long)id * p.rows_per_block + kvh * HY_KV_BLOCK_TOKENS;
-#pragma unroll
-            for (int c = 0; c < C::NC; ++c) {
-              tma_prefetch_2d(&tmKV, c * 64, (int)row);
-              tma_prefetch_2d(&tmKV, c * 64, (int)(row + p.rows_per_kv));
-            }
-          }
+        for (int c = 0; c < C::NC; ++c) {
+          tma_prefetch_2d(&tmKV, c * 64, (int)row);
+          tma_prefetch_2d(&tmKV, c * 64, (int)(row + p.rows_per_kv));
         }
       }
       ids = next;
