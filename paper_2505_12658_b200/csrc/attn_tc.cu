@@ -110,12 +110,14 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
   uint8_t* sKV = smem + C::TILES * C::Q_BYTES;      // stage s: K at s * STAGE, V at + KV_BYTES
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + 2 * C::STAGE_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2 stages]
-  uint64_t* kv_empty = bars + 3;  // [2 stages]
-  uint64_t* s_full = bars + 5;    // [2 tiles]
-  uint64_t* p_full = bars + 7;    // [2 tiles]
-  uint64_t* o_done = bars + 9;    // [2 tiles]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* k_full = bars + 1;    // [2 stages]  K and V of a stage are tracked separately:
+  uint64_t* k_empty = bars + 3;   // [2 stages]  K is retired after the Q K^T MMAs, long
+  uint64_t* v_full = bars + 5;    // [2 stages]  before V (after P V), so the next-but-one
+  uint64_t* v_empty = bars + 7;   // [2 stages]  K tile loads a softmax earlier
+  uint64_t* s_full = bars + 9;    // [2 tiles]
+  uint64_t* p_full = bars + 11;   // [2 tiles]
+  uint64_t* o_done = bars + 13;   // [2 tiles]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -124,8 +126,10 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
     tma_prefetch_desc(&tmKV);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
       mbar_init(&o_done[i], 1);
@@ -161,32 +165,43 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
       if (PAGED && lane < BPT && j + 1 < n_kt) next = bt[min((j + 1) * BPT + lane, last_blk)];
       uint8_t* sK = sKV + st * C::STAGE_BYTES;
       uint8_t* sV = sK + C::KV_BYTES;
+      const long long row = PAGED ? (long long)ids * p.rows_per_block + kvh * HY_KV_BLOCK_TOKENS : 0;
+      // K_j (lane b: block b of the tile; eight lanes drive the TMA unit in parallel)
       if (lane == 0) {
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
         ATR(0, j);
-        mbar_expect_tx(&kv_full[st], C::STAGE_BYTES);
+        mbar_expect_tx(&k_full[st], C::KV_BYTES);
       }
-      __syncwarp();  // expect_tx (lane 0) precedes every lane's loads on this barrier
+      __syncwarp();
       if (PAGED) {
-        // lane b issues block b's boxes: eight lanes drive the TMA unit in parallel
-        if (lane < BPT) {
-          const long long row = (long long)ids * p.rows_per_block + kvh * HY_KV_BLOCK_TOKENS;
+        if (lane < BPT)
 #pragma unroll
-          for (int c = 0; c < C::NC; ++c) {
-            tma_load_2d(&tmKV, &kv_full[st], sK + c * C::CHUNK + lane * 2048, c * 64, (int)row,
+          for (int c = 0; c < C::NC; ++c)
+            tma_load_2d(&tmKV, &k_full[st], sK + c * C::CHUNK + lane * 2048, c * 64, (int)row,
                         kEvictNormal);
-            tma_load_2d(&tmKV, &kv_full[st], sV + c * C::CHUNK + lane * 2048, c * 64,
-                        (int)(row + p.rows_per_kv), kEvictNormal);
-          }
-        }
       } else if (lane == 0) {
 #pragma unroll
-        for (int c = 0; c < C::NC; ++c) {
-          tma_load_2d(&tmKV, &kv_full[st], sK + c * C::CHUNK, p.k_col0 + kvh * D + c * 64,
+        for (int c = 0; c < C::NC; ++c)
+          tma_load_2d(&tmKV, &k_full[st], sK + c * C::CHUNK, p.k_col0 + kvh * D + c * 64,
                       q0 + j * C::BK, kEvictNormal);
-          tma_load_2d(&tmKV, &kv_full[st], sV + c * C::CHUNK, p.v_col0 + kvh * D + c * 64,
+      }
+      // V_j
+      if (lane == 0) {
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], C::KV_BYTES);
+      }
+      __syncwarp();
+      if (PAGED) {
+        if (lane < BPT)
+#pragma unroll
+          for (int c = 0; c < C::NC; ++c)
+            tma_load_2d(&tmKV, &v_full[st], sV + c * C::CHUNK + lane * 2048, c * 64,
+                        (int)(row + p.rows_per_kv), kEvictNormal);
+      } else if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < C::NC; ++c)
+          tma_load_2d(&tmKV, &v_full[st], sV + c * C::CHUNK, p.v_col0 + kvh * D + c * 64,
                       q0 + j * C::BK, kEvictNormal);
-        }
       }
       // warm L2 with the next tile's blocks: its TMA loads (issued once a stage frees up)
       // then hit L2 instead of HBM -- the 32 small boxes per tile are latency-bound
@@ -222,6 +237,7 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
         umma_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int j) {
+        if (t == 0) mbar_wait(&v_full[j & 1], (j >> 1) & 1);
         mbar_wait(&p_full[t], j & 1);
         ATR(2 + t, j);
         tc_fence_after();
@@ -234,24 +250,26 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
         umma_commit(&o_done[t]);
       };
       mbar_wait(q_full, 0);
-      mbar_wait(&kv_full[0], 0);
+      mbar_wait(&k_full[0], 0);
       tc_fence_after();
       issue_s(0, 0);
       issue_s(1, 0);
+      umma_commit(&k_empty[0]);  // K_0 retired once both Q K^T complete
       for (int j = 0; j < n_kt; ++j) {
         const bool more = j + 1 < n_kt;
         for (int t = 0; t < C::TILES; ++t) {
           issue_pv(t, j);
           if (more) {
             if (t == 0) {  // the next key tile is needed only from here on
-              mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+              mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
               ATR(1, j + 1);
               tc_fence_after();
             }
             issue_s(t, j + 1);
           }
         }
-        umma_commit(&kv_empty[j & 1]);  // K_j and V_j retired once these MMAs complete
+        if (more) umma_commit(&k_empty[(j + 1) & 1]);
+        umma_commit(&v_empty[j & 1]);  // V_j retired once both P V complete
       }
     }
   } else {
