@@ -49,6 +49,27 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// packed fp32x2 FMA / add (FFMA2 / FADD2: two lanes of math per issue slot -- the softmax
+// is issue-bound once the S row is in registers)
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 struct TcAttnParams {
   const int* qstart;   // [n_seqs + 1] query rows of each sequence in the Q map
   const int* offset;   // paged: tokens cached before the chunk
@@ -338,26 +359,31 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
       const float ms = m_used == -INFINITY ? 0.f : m_used;
       // P_t = exp2(S * scale - m) as bf16 pairs into S_t's first 64 columns (A of PV), 16
       // columns per store; column c of P holds keys 2c, 2c+1 (already in registers)
-      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-      const float sc = p.scale_log2;
+      uint64_t rs2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
+      const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2), nms2 = pk2(-ms, -ms);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           const int k0 = c * 32 + 2 * u;
-          float e0 = ex2_approx(fmaf(__uint_as_float(r[k0]), sc, -ms));
-          float e1 = ex2_approx(fmaf(__uint_as_float(r[k0 + 1]), sc, -ms));
+          float x0, x1;
+          up2(ffma2(pk2(__uint_as_float(r[k0]), __uint_as_float(r[k0 + 1])), sc2, nms2), x0, x1);
+          float e0 = ex2_approx(x0);
+          float e1 = ex2_approx(x1);
           if (!full) {
             e0 = kbase + k0 < kmax ? e0 : 0.f;
             e1 = kbase + k0 + 1 < kmax ? e1 : 0.f;
           }
-          rs4[u & 3] += e0 + e1;
+          rs2[u & 1] = fadd2(rs2[u & 1], pk2(e0, e1));
           pk[u] = pack_bf16x2(e0, e1);
         }
         tmem_st_32x32b_x16(tS + c * 16, pk);
       }
-      const float rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+      float ra, rb, rc, rd;
+      up2(rs2[0], ra, rb);
+      up2(rs2[1], rc, rd);
+      const float rs = (ra + rb) + (rc + rd);
       l += rs;
       tmem_st_wait();
       tc_fence_before();

@@ -22,6 +22,13 @@ int main(int argc, char** argv) {
     if (rc) { printf("rc %d %s\n", rc, hy::get_last_error()); return 1; }
   }
   cudaDeviceSynchronize();
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int it = 0; it < 20; ++it)
+    hy::attn_tc_prefill(q, nh * d, c, 1, qs, offs, slots, c, nh, nh, d, bt, nb, kv, be, 0.088f, o, nh * d, 0);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  printf("avg %.1f us  (%.0f TF/s)\n", ms * 1000 / 20, 4.0 * d * nh * (double)c * (c + 1) / 2 / (ms / 20 * 1e-3) / 1e12);
   unsigned long long tr[8][64];
   cudaMemcpyFromSymbol(tr, hy::g_atrace, sizeof(tr));
   unsigned long long t0 = tr[0][0];
