@@ -329,7 +329,7 @@ def run_ours(args, d: Dist):
         e2e_rate = None
         e2e_probes = []
         img_bytes = shape.patch_grid(576)[0] * shape.patch_grid(576)[1] * shape.patch ** 2 * 3
-        for f in (1.0, 0.85, 0.7, 0.5):
+        for f in (1.0, 0.96, 0.92, 0.88, 0.8, 0.6):
             r = best * f
             cl, rep = replay(r * d.world, clock="wall", resident=False)
             meets = sum(1 for m in rep.requests if P.epdsim.meets_slo(m))
