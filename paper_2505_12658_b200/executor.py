@@ -136,7 +136,8 @@ class InstanceRuntime:
         self.exec_log: List[Dict] = []
         self.sampler = None  # profiling.KernelSampler (bench.py)
         self.stats = {"batches": 0, "lang_rows": 0, "decode_rows": 0, "prefill_rows": 0,
-                      "images": 0, "device_ms": 0.0, "host_ms": 0.0, "mixed_batches": 0,
+                      "images": 0, "device_ms": 0.0, "host_ms": 0.0, "prep_ms": 0.0,
+                      "launch_ms": 0.0, "mixed_batches": 0,
                       "vision_critical": 0}
 
     # ------------------------------------------------------------------ helpers
@@ -352,6 +353,7 @@ class InstanceRuntime:
                 cap_logits = torch.empty((n_out, self.shape.vocab), dtype=torch.float32,
                                          device=dev)
                 logits_ptr = cap_logits.data_ptr()
+            self.stats["prep_ms"] += (time.perf_counter() - t_host0) * 1e3
             lb = _lib.HyLangBatch(n_rows, nd, npf, ptrs["tok"], ptrs["pos"], ptrs["row_slot"],
                                   ptrs["dec_ctx"], ptrs["pf_qstart"], ptrs["pf_offset"],
                                   ptrs["pf_slot"], max_q, max(max_ctx, 1), n_out,
@@ -363,6 +365,7 @@ class InstanceRuntime:
             self.stats["lang_rows"] += n_rows
             self.stats["decode_rows"] += nd
             self.stats["prefill_rows"] += n_rows - nd
+        self.stats["launch_ms"] += (time.perf_counter() - t_host0) * 1e3
         if has_vis:
             self._run_vision(batch, reqs, sv)
         self.ev_l.record(sl)

@@ -251,7 +251,8 @@ def test_vit_varlen_attention(d, lens):
         r0 += n
 
 
-def test_rope_kv_append():
+@pytest.mark.parametrize("pad", [0, 4])  # pad 4: ld_qkv % 8 != 0 -> 4-byte (scalar) path
+def test_rope_kv_append(pad):
     nh, nkv, d, L, layer = 4, 2, 128, 3, 2
     R = 40
     pos = torch.tensor(list(range(0, 20)) + list(range(100, 120)), dtype=torch.int32, device=DEV)
@@ -260,10 +261,11 @@ def test_rope_kv_append():
                       device=DEV)
     be = L * 2 * nkv * 16 * d
     kv = torch.zeros(10, be, dtype=torch.bfloat16, device=DEV)
-    qkv = torch.randn(R, (nh + 2 * nkv) * d, device=DEV).bfloat16()
+    qkv_full = torch.randn(R, (nh + 2 * nkv) * d + pad, device=DEV).bfloat16()
+    qkv = qkv_full[:, :(nh + 2 * nkv) * d]
     q0 = qkv.clone()
     layer_ptr = kv.data_ptr() + layer * 2 * nkv * 16 * d * 2
-    ck(lib().hy_rope_kv_append(qkv.data_ptr(), qkv.shape[1], R, nh, nkv, d, pos.data_ptr(),
+    ck(lib().hy_rope_kv_append(qkv.data_ptr(), qkv_full.shape[1], R, nh, nkv, d, pos.data_ptr(),
                                slot.data_ptr(), bt.data_ptr(), 8, layer_ptr, be, 10000.0, st()))
     inv = 1.0 / (10000.0 ** (torch.arange(0, d // 2, device=DEV).float() * 2 / d))
     ang = pos.float()[:, None] * inv[None]
@@ -274,7 +276,7 @@ def test_rope_kv_append():
         return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1)
 
     x = q0.float().view(R, nh + 2 * nkv, d)
-    assert (qkv.float().view(R, -1, d)[:, :nh] - rope(x[:, :nh])).abs().max() < 2e-2
+    assert (qkv.float().reshape(R, -1, d)[:, :nh] - rope(x[:, :nh])).abs().max() < 2e-2
     lay = kv.view(10, L, 2, nkv, 16, d)[:, layer]
     for r in range(R):
         p = int(pos[r]); b = int(bt[int(slot[r]), p // 16])

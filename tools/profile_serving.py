@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--rate", type=float, default=60.0)
     ap.add_argument("--model", default="llava-1.5-7b")
     ap.add_argument("--budgets", default="roofline", choices=["roofline", "measured"])
+    ap.add_argument("--clock", default="device", choices=["device", "wall"])
     ap.add_argument("--watchdog", type=float, default=0.0,
                     help="dump Python stacks and exit after this many seconds (hang triage)")
     args = ap.parse_args()
@@ -37,13 +38,17 @@ def main():
                        visual_token_choices=576, prompt_dist=[25, 35, 45],
                        output_dist=[90, 110, 130], slo=slo)
     spec = C.ClusterSpec(method=C.DisaggregationMethod.parse("EPD:1"))
-    cl = GpuCluster(spec, shape, P.b200_hardware(), slo, clock="device",
-                    budgets=args.budgets)
+    cl = GpuCluster(spec, shape, P.b200_hardware(), slo, clock=args.clock,
+                    budgets=args.budgets, resident_inputs=args.clock == "device")
     rep = cl.run(tr)
     torch.cuda.synchronize()
     rt = next(iter(cl.runtimes.values()))
+    nb = max(1, rt.stats["batches"])
     print("batches", rt.stats["batches"], "device_ms", round(rt.stats["device_ms"], 1),
           "attainment", rep.aggregates["slo_attainment"])
+    print("per batch ms: device %.2f host %.2f prep(lang lowering) %.2f lang-launch-done %.2f"
+          % (rt.stats["device_ms"] / nb, rt.stats["host_ms"] / nb, rt.stats["prep_ms"] / nb,
+             rt.stats["launch_ms"] / nb))
 
 
 if __name__ == "__main__":
