@@ -158,6 +158,126 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// GQA variant (G >= 4 query heads per KV head): the four warps split the G heads (GW =
+// ceil(G / 4) each) and every warp streams the whole KV range, so each lane keeps only GW
+// heads of q / accumulators in registers (the G = 7 instance of attn_decode_kernel needed
+// 255 registers and spilled, running at ~20% of HBM bandwidth).  The four warps read the
+// same lines at about the same time: loads allocate in L1 and HBM sees each byte once.
+template <int GW>
+__global__ void __launch_bounds__(128)
+    attn_decode_gqa_kernel(const bf16* __restrict__ q, int ld_q, int n_kv, int G,
+                           const int* __restrict__ slots, const int* __restrict__ ctx_len,
+                           const int* __restrict__ block_table, int bt_stride,
+                           const bf16* __restrict__ kv, long long block_stride, float scale_log2,
+                           int blocks_per_split, bf16* __restrict__ out, int ld_o,
+                           float* __restrict__ part, int nsplit) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int D = 128;
+  const int b = blockIdx.x, kh = blockIdx.y, sp = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, dl = lane & 15;
+  const int n_heads = n_kv * G;
+  const int g0 = warp * GW;  // first head (within the group) of this warp
+  const int ng = min(GW, G - g0);
+  if (ng <= 0) return;
+  const int ctx = ctx_len[b];
+  const int nblk = (ctx + HY_KV_BLOCK_TOKENS - 1) / HY_KV_BLOCK_TOKENS;
+  const int blk0 = sp * blocks_per_split;
+  const int blk1 = min(nblk, blk0 + blocks_per_split);
+  const int* bt = block_table + (size_t)slots[b] * bt_stride;
+  float qf[GW][8], m[GW], l[GW], acc[GW][8];
+#pragma unroll
+  for (int g = 0; g < GW; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[g][j] = 0.f;
+    if (g < ng) {
+      load_bf16x8(q + (size_t)b * ld_q + (size_t)(kh * G + g0 + g) * D + dl * 8, qf[g]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) qf[g][j] *= scale_log2;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) qf[g][j] = 0.f;
+    }
+  }
+  const size_t head_off = (size_t)kh * HY_KV_BLOCK_TOKENS * D;
+  const size_t v_off = (size_t)n_kv * HY_KV_BLOCK_TOKENS * D;
+  for (int jb = blk0; jb < blk1; ++jb) {
+    const bf16* kb = kv + (size_t)bt[jb] * block_stride + head_off;
+    const bf16* vb = kb + v_off;
+    uint4 kr[8], vr[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) kr[i] = *reinterpret_cast<const uint4*>(kb + (size_t)(2 * i + half) * D + dl * 8);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) vr[i] = *reinterpret_cast<const uint4*>(vb + (size_t)(2 * i + half) * D + dl * 8);
+    const int tok_base = jb * HY_KV_BLOCK_TOKENS + half;
+#pragma unroll
+    for (int g = 0; g < GW; ++g) {
+      float s[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float2 k0 = unpack_bf16x2(kr[i].x), k1 = unpack_bf16x2(kr[i].y),
+               k2 = unpack_bf16x2(kr[i].z), k3 = unpack_bf16x2(kr[i].w);
+        float d0 = qf[g][0] * k0.x + qf[g][1] * k0.y + qf[g][2] * k1.x + qf[g][3] * k1.y +
+                   qf[g][4] * k2.x + qf[g][5] * k2.y + qf[g][6] * k3.x + qf[g][7] * k3.y;
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 8);
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 4);
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
+        s[i] = (tok_base + 2 * i < ctx) ? d0 : -INFINITY;
+      }
+      float mb = s[0];
+#pragma unroll
+      for (int i = 1; i < 8; ++i) mb = fmaxf(mb, s[i]);
+      mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
+      const float mn = fmaxf(m[g], mb);  // finite: every block holds >= 1 valid token
+      const float corr = exp2f(m[g] - mn);
+      m[g] = mn;
+      float ls = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[g][j] *= corr;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float p = exp2f(s[i] - mn);
+        ls += p;
+        float2 v0 = unpack_bf16x2(vr[i].x), v1 = unpack_bf16x2(vr[i].y),
+               v2 = unpack_bf16x2(vr[i].z), v3 = unpack_bf16x2(vr[i].w);
+        acc[g][0] += p * v0.x; acc[g][1] += p * v0.y;
+        acc[g][2] += p * v1.x; acc[g][3] += p * v1.y;
+        acc[g][4] += p * v2.x; acc[g][5] += p * v2.y;
+        acc[g][6] += p * v3.x; acc[g][7] += p * v3.y;
+      }
+      l[g] = l[g] * corr + ls;
+    }
+  }
+  // merge the two half-warps (same m, disjoint tokens) and write this warp's heads
+#pragma unroll
+  for (int g = 0; g < GW; ++g) {
+    l[g] += __shfl_xor_sync(0xffffffffu, l[g], 16);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[g][j] += __shfl_xor_sync(0xffffffffu, acc[g][j], 16);
+    if (g >= ng || half != 0) continue;
+    const int hq = kh * G + g0 + g;
+    if (nsplit == 1) {
+      float o[8];
+      const float inv = l[g] > 0.f ? 1.f / l[g] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = acc[g][j] * inv;
+      store_bf16x8(out + (size_t)b * ld_o + (size_t)hq * D + dl * 8, o);
+    } else {
+      float* pp = part + (((size_t)b * n_heads + hq) * nsplit + sp) * (D + 2);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) pp[dl * 8 + j] = acc[g][j];
+      if (dl == 0) {
+        pp[D] = m[g];
+        pp[D + 1] = l[g];
+      }
+    }
+  }
+}
+
 __global__ void attn_decode_combine_kernel(const float* __restrict__ part, int n_heads, int nsplit,
                                            bf16* __restrict__ out, int ld_o) {
   pdl_trigger();
@@ -222,7 +342,20 @@ extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads,
                                                      block_table, bt_stride, kvp, block_stride, \
                                                      sl2, bps, op, ld_o, part, ns));            \
     break;
-  switch (G) {
+  if (G >= 4 && G <= 16 && !getenv("HY_DECODE_GQA_OFF")) {
+    // warps split the heads: GW = ceil(G / 4) heads per warp
+    auto launch_gqa = [&](auto kern) {
+      return launch_pdl(kern, dim3(grid), dim3(128), 0, stream, qp, ld_q, n_kv_heads, G, slots,
+                        ctx, block_table, bt_stride, kvp, block_stride, sl2, bps, op, ld_o, part,
+                        ns);
+    };
+    if (G <= 4)
+      HY_CUDA_RET(launch_gqa(attn_decode_gqa_kernel<1>));
+    else if (G <= 8)
+      HY_CUDA_RET(launch_gqa(attn_decode_gqa_kernel<2>));
+    else
+      HY_CUDA_RET(launch_gqa(attn_decode_gqa_kernel<4>));
+  } else switch (G) {
     HY_DEC_CASE(1)
     HY_DEC_CASE(2)
     HY_DEC_CASE(4)

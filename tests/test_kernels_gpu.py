@@ -167,7 +167,9 @@ def _gather_kv(kv, bt, i, ctx, n_layers, layer, n_kv, d):
 @pytest.mark.parametrize("n_heads,n_kv,ctxs", [
     (4, 4, [1, 17, 300, 33]),
     (32, 32, [616, 617, 2000]),
-    (28, 4, [5, 900, 4097]),          # GQA group 7 (Qwen2-VL)
+    (28, 4, [5, 900, 4097]),          # GQA group 7 (Qwen2-VL): warps split the heads
+    (32, 4, [1, 300, 2000]),          # GQA group 8
+    (16, 4, [33, 17]),                # GQA group 4
     (8, 8, [16 * 64 * 3 + 5]),        # long context: split-KV combine path
 ])
 def test_decode_attention(n_heads, n_kv, ctxs):

@@ -271,6 +271,39 @@ def overlap_probe(out):
           flush=True)
 
 
+def decode_sweep(out):
+    """Paged decode attention (K8) bandwidth for MHA (LLaVA) and GQA (Qwen2-VL 28/4)."""
+    import math
+    for nh, nkv, n, ctx in ((32, 32, 256, 660), (28, 4, 256, 660), (28, 4, 64, 4000),
+                            (32, 8, 256, 660), (32, 32, 16, 8000)):
+        d = 128
+        nb = -(-ctx // 16)
+        be = 2 * nkv * 16 * d
+        kv = torch.randn(n * nb + 1, be, device=DEV).bfloat16()
+        bt = torch.arange(n * nb, dtype=torch.int32, device=DEV).view(n, nb).contiguous()
+        q = torch.randn(n, nh * d, device=DEV).bfloat16()
+        o = torch.empty_like(q)
+        slots = torch.arange(n, dtype=torch.int32, device=DEV)
+        ctxs = torch.full((n,), ctx, dtype=torch.int32, device=DEV)
+        wsb = lib().hy_attn_decode_workspace_bytes(n, nh, d, ctx)
+        ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=DEV)
+
+        def ours(i):
+            rc = lib().hy_attn_decode_paged(q.data_ptr(), nh * d, n, nh, nkv, d, slots.data_ptr(),
+                                            ctxs.data_ptr(), ctx, bt.data_ptr(), nb, kv.data_ptr(),
+                                            be, 1 / math.sqrt(d), o.data_ptr(), nh * d,
+                                            ws.data_ptr(), ws.numel(), st())
+            assert rc == 0, lib().hy_last_error()
+        t = timeit(ours)
+        byt = n * ctx * 2 * nkv * d * 2
+        r = {"name": "decode_attn", "n_heads": nh, "n_kv": nkv, "seqs": n, "ctx": ctx,
+             "us": t * 1e3, "gbs": byt / t / 1e6}
+        out.append(r)
+        print(f"decode_attn heads {nh}/{nkv} seqs {n} ctx {ctx}: {t*1e3:8.1f} us "
+              f"{r['gbs']:7.0f} GB/s", flush=True)
+        del kv
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--what", default="gemm")
@@ -293,6 +326,9 @@ def main():
     if "attn" in args.what:
         res["attn"] = []
         attn_sweep(res["attn"])
+    if "decode" in args.what:
+        res["decode"] = []
+        decode_sweep(res["decode"])
     if "overlap" in args.what:
         res["overlap"] = []
         overlap_probe(res["overlap"])
