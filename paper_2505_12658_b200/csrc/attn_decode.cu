@@ -15,6 +15,7 @@
 // context is split across CTAs (flash-decoding) a second kernel merges the partials.
 #include "common.cuh"
 #include "../../include/hydra_sm100.h"
+#include "mma_sync.cuh"
 
 #include <algorithm>
 
@@ -278,6 +279,199 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// GQA on tensor cores (G >= 4 query heads per KV head): the G heads of one KV head are the
+// (zero-padded) 16 rows of an mma.sync m16n8k16 tile, so each 16-token cache block costs
+// 16 + 16 MMAs instead of G x 16 x 128 CUDA-core FMAs plus shuffles -- the CUDA-core
+// kernels above are compute/shuffle-bound at G = 7 (~1.7 TB/s).  Warps split the blocks
+// (like the MHA kernel); each warp double-buffers its K/V blocks in shared memory with
+// cp.async, S = Q K^T and O += P V run on the tensor pipe with the FA2 register reuse of
+// the S accumulators as the P operand, online softmax in the exp2 domain; warps merge
+// through shared memory, split-KV partials go through the combine kernel.
+constexpr int GQ_LDS = 128 + 8;  // padded bf16 row: conflict-free ldmatrix
+constexpr int GQ_SMEM = (16 + DEC_WARPS * 4 * 16) * GQ_LDS * 2;  // Q + per warp 2x(K, V)
+__global__ void __launch_bounds__(128)
+    attn_decode_gqa_mma_kernel(const bf16* __restrict__ q, int ld_q, int n_kv, int G,
+                               const int* __restrict__ slots, const int* __restrict__ ctx_len,
+                               const int* __restrict__ block_table, int bt_stride,
+                               const bf16* __restrict__ kv, long long block_stride,
+                               float scale_log2, int blocks_per_split, bf16* __restrict__ out,
+                               int ld_o, float* __restrict__ part, int nsplit) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int D = 128, LDS = GQ_LDS, CPR = D / 8;
+  extern __shared__ __align__(128) uint8_t gq_smem[];
+  bf16* sQ = reinterpret_cast<bf16*>(gq_smem);
+  const int b = blockIdx.x, kh = blockIdx.y, sp = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_heads = n_kv * G;
+  const int ctx = ctx_len[b];
+  const int nblk = (ctx + HY_KV_BLOCK_TOKENS - 1) / HY_KV_BLOCK_TOKENS;
+  const int blk0 = sp * blocks_per_split;
+  const int blk1 = min(nblk, blk0 + blocks_per_split);
+  const int* bt = block_table + (size_t)slots[b] * bt_stride;
+  bf16* sK = sQ + 16 * LDS + warp * 4 * 16 * LDS;  // [2 bufs][16][LDS]
+  bf16* sV = sK + 2 * 16 * LDS;
+  // Q rows: the G heads of this KV head (rows >= G zero)
+  for (int c = tid; c < 16 * CPR; c += 128) {
+    const int r = c / CPR, col = (c % CPR) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < G) v = *reinterpret_cast<const uint4*>(q + (size_t)b * ld_q + (size_t)(kh * G + r) * D + col);
+    *reinterpret_cast<uint4*>(sQ + r * LDS + col) = v;
+  }
+  const size_t head_off = (size_t)kh * HY_KV_BLOCK_TOKENS * D;
+  const size_t v_off = (size_t)n_kv * HY_KV_BLOCK_TOKENS * D;
+  auto load_block = [&](int jb, int buf) {
+    const bf16* kb = kv + (size_t)bt[jb] * block_stride + head_off;
+    const bf16* vb = kb + v_off;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int c = lane + i * 32;  // 256 16-byte pieces per 16 x 128 block
+      const int r = c / CPR, col = (c % CPR) * 8;
+      cp_async16(sK + buf * 16 * LDS + r * LDS + col, kb + (size_t)r * D + col, true);
+      cp_async16(sV + buf * 16 * LDS + r * LDS + col, vb + (size_t)r * D + col, true);
+    }
+  };
+  __syncthreads();
+  uint32_t qf[8][4];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int row = (lane & 7) + ((lane >> 3) & 1) * 8;
+    const int col = kk * 16 + (lane >> 4) * 8;
+    ldsm_x4(smem_u32(sQ + row * LDS + col), qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
+  }
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows lane/4 and lane/4 + 8
+  int jb = blk0 + warp;
+  if (jb < blk1) load_block(jb, 0);
+  cp_async_commit();
+  for (int it = 0; jb < blk1; jb += DEC_WARPS, ++it) {
+    const int buf = it & 1;
+    if (jb + DEC_WARPS < blk1) load_block(jb + DEC_WARPS, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const bf16* cK = sK + buf * 16 * LDS;
+    const bf16* cV = sV + buf * 16 * LDS;
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int key = (lane & 7) + (lane >> 4) * 8;
+      const int col = kk * 16 + ((lane >> 3) & 1) * 8;
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(smem_u32(cK + key * LDS + col), b0, b1, b2, b3);
+      mma_bf16_16816(s[0], qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b0, b1);
+      mma_bf16_16816(s[1], qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b2, b3);
+    }
+    // scale, mask, online softmax (row lo: s[.][0..1], row hi: s[.][2..3])
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tok = jb * HY_KV_BLOCK_TOKENS + nt * 8 + (lane & 3) * 2 + e;
+        const bool ok = tok < ctx;
+        s[nt][e] = ok ? s[nt][e] * scale_log2 : -INFINITY;
+        s[nt][2 + e] = ok ? s[nt][2 + e] * scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, s[nt][e]);
+        mx1 = fmaxf(mx1, s[nt][2 + e]);
+      }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);  // finite: block has a valid token
+    const float c0 = exp2f(m0 - mn0), c1 = exp2f(m1 - mn1);
+    m0 = mn0;
+    m1 = mn1;
+    float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      s[nt][0] = exp2f(s[nt][0] - mn0);
+      s[nt][1] = exp2f(s[nt][1] - mn0);
+      s[nt][2] = exp2f(s[nt][2] - mn1);
+      s[nt][3] = exp2f(s[nt][3] - mn1);
+      rs0 += s[nt][0] + s[nt][1];
+      rs1 += s[nt][2] + s[nt][3];
+    }
+    l0 = l0 * c0 + rs0;
+    l1 = l1 * c1 + rs1;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      o[i][0] *= c0;
+      o[i][1] *= c0;
+      o[i][2] *= c1;
+      o[i][3] *= c1;
+    }
+    const uint32_t a0 = pack_bf16x2(s[0][0], s[0][1]), a1 = pack_bf16x2(s[0][2], s[0][3]);
+    const uint32_t a2 = pack_bf16x2(s[1][0], s[1][1]), a3 = pack_bf16x2(s[1][2], s[1][3]);
+#pragma unroll
+    for (int dp = 0; dp < 8; ++dp) {
+      const int key = (lane & 7) + ((lane >> 3) & 1) * 8;
+      const int col = dp * 16 + (lane >> 4) * 8;
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(smem_u32(cV + key * LDS + col), b0, b1, b2, b3);
+      mma_bf16_16816(o[2 * dp], a0, a1, a2, a3, b0, b1);
+      mma_bf16_16816(o[2 * dp + 1], a0, a1, a2, a3, b2, b3);
+    }
+    __syncwarp();  // this buffer is refilled two iterations later
+  }
+  cp_async_wait<0>();
+  // row sums over the 4 lanes sharing a row
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  // merge warps through shared memory (reuses the K/V buffers)
+  __syncthreads();
+  float* sO = reinterpret_cast<float*>(gq_smem);            // [4][16][128]
+  float* sM = sO + DEC_WARPS * 16 * D;                       // [4][16]
+  float* sL = sM + DEC_WARPS * 16;                           // [4][16]
+  const int r0 = lane >> 2, r1 = r0 + 8;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int col = i * 8 + (lane & 3) * 2;
+    sO[(warp * 16 + r0) * D + col] = o[i][0];
+    sO[(warp * 16 + r0) * D + col + 1] = o[i][1];
+    sO[(warp * 16 + r1) * D + col] = o[i][2];
+    sO[(warp * 16 + r1) * D + col + 1] = o[i][3];
+  }
+  if ((lane & 3) == 0) {
+    sM[warp * 16 + r0] = m0;
+    sM[warp * 16 + r1] = m1;
+    sL[warp * 16 + r0] = l0;
+    sL[warp * 16 + r1] = l1;
+  }
+  __syncthreads();
+  for (int e = tid; e < G * D; e += blockDim.x) {
+    const int g = e / D, d = e % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < DEC_WARPS; ++w) M = fmaxf(M, sM[w * 16 + g]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < DEC_WARPS; ++w) {
+        const float f = exp2f(sM[w * 16 + g] - M);
+        L += sL[w * 16 + g] * f;
+        O += sO[(w * 16 + g) * D + d] * f;
+      }
+    }
+    const int hq = kh * G + g;
+    if (nsplit == 1) {
+      out[(size_t)b * ld_o + (size_t)hq * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
+    } else {
+      float* pp = part + (((size_t)b * n_heads + hq) * nsplit + sp) * (D + 2);
+      pp[d] = O;
+      if (d == 0) {
+        pp[D] = M;
+        pp[D + 1] = L;
+      }
+    }
+  }
+}
+
 __global__ void attn_decode_combine_kernel(const float* __restrict__ part, int n_heads, int nsplit,
                                            bf16* __restrict__ out, int ld_o) {
   pdl_trigger();
@@ -342,7 +536,19 @@ extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads,
                                                      block_table, bt_stride, kvp, block_stride, \
                                                      sl2, bps, op, ld_o, part, ns));            \
     break;
-  if (G >= 4 && G <= 16 && !getenv("HY_DECODE_GQA_OFF")) {
+  if (G >= 4 && G <= 16 && !getenv("HY_DECODE_GQA_CUDA")) {
+    static bool attr = false;
+    if (!attr) {
+      HY_CUDA_RET(cudaFuncSetAttribute(attn_decode_gqa_mma_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       std::max(GQ_SMEM, (DEC_WARPS * 16 * 130 + 64) * 4)));
+      attr = true;
+    }
+    HY_CUDA_RET(launch_pdl(attn_decode_gqa_mma_kernel, dim3(grid), dim3(128),
+                           (size_t)std::max(GQ_SMEM, (DEC_WARPS * 16 * 130 + 64) * 4), stream,
+                           qp, ld_q, n_kv_heads, G, slots, ctx, block_table, bt_stride, kvp,
+                           block_stride, sl2, bps, op, ld_o, part, ns));
+  } else if (G >= 4 && G <= 16) {
     // warps split the heads: GW = ceil(G / 4) heads per warp
     auto launch_gqa = [&](auto kern) {
       return launch_pdl(kern, dim3(grid), dim3(128), 0, stream, qp, ld_q, n_kv_heads, G, slots,
