@@ -575,7 +575,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
-  const int T = a.np * a.nq;
   if (!(a.dbg & 1)) pdl_trigger();
 
   if (warp == 0 && lane == 0) {
@@ -596,6 +595,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  long long su0, su1;
+  const int nseg = cta_segments(a, pair, npairs, su0, su1);  // data-parallel + stream-K
 
   if (warp == 0) {
     if (lane == 0) {
@@ -612,19 +613,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
       };
       // weights of the first stages before the grid dependency resolves
       int npre = 0;
-      for (int t = pair; t < T && npre < C::STAGES; t += npairs) {
+      for (int i = 0; i < nseg && npre < C::STAGES; ++i) {
+        const Seg sg = get_segment(a, pair, npairs, i, su0, su1);
         int p, q;
-        raster_tile(t, a, p, q);
-        for (int kb = 0; kb < a.nkb && npre < C::STAGES; ++kb, ++npre) load_w(npre, kb, q);
+        raster_tile(sg.tile, a, p, q);
+        for (int kb = sg.kb0; kb < sg.kb1 && npre < C::STAGES; ++kb, ++npre) load_w(npre, kb, q);
       }
       pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       int g = 0;
-      for (int t = pair; t < T; t += npairs) {
+      for (int i = 0; i < nseg; ++i) {
+        const Seg sg = get_segment(a, pair, npairs, i, su0, su1);
         int p, q;
-        raster_tile(t, a, p, q);
-        for (int kb = 0; kb < a.nkb; ++kb, ++g) {
+        raster_tile(sg.tile, a, p, q);
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++g) {
           if (g < npre) {
             load_x(stage, kb, p);
           } else {
@@ -647,11 +650,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = pair; t < T; t += npairs) {
+      for (int i = 0; i < nseg; ++i) {
+        const Seg sg = get_segment(a, pair, npairs, i, su0, su1);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < a.nkb; ++kb) {
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
@@ -659,7 +663,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
 #pragma unroll
           for (int k = 0; k < C::BK / 16; ++k)
             umma_bf16_cg2(d_tmem, smem_desc_k_sw128(a_addr + k * 32),
-                          smem_desc_k_sw128(b_addr + k * 32), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                          smem_desc_k_sw128(b_addr + k * 32), idesc,
+                          (kb > sg.kb0 || k > 0) ? 1u : 0u);
           umma_commit_cg2(&empty[stage], 0x3);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -681,21 +686,77 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = pair; t < T; t += npairs) {
+    for (int i = 0; i < nseg; ++i) {
+      const Seg sg = get_segment(a, pair, npairs, i, su0, su1);
       int p, q;
-      raster_tile(t, a, p, q);
+      raster_tile(sg.tile, a, p, q);
       mbar_wait_sleepy(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN;
+      const int lrow = sub * 32 + lane;  // this CTA's accumulator row (TMEM lane)
+      bool finish = true;
+      int c0 = 0, c1 = -1;
+      long long ub = 0;
+      if (sg.slot >= 0) {
+        // stream-K partial of this CTA's 128 rows: [pair][slot][rank][chunk][j/4][row] float4
+        float4* mine = reinterpret_cast<float4*>(a.partial) +
+                       ((size_t)(pair * 2 + sg.slot) * 2 + rank) * (BN / 32) * 8 * 128 + lrow;
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + c * 32, r);
-        tmem_ld_wait();
-        float v[32];
+        for (int c = half; c < BN / 32; c += 2) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + c * 32, r);
+          tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        epi_chunk<EPI, false>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32, v, lane, 0u);
+          for (int j = 0; j < 32; j += 4)
+            __stcg(mine + (c * 8 + j / 4) * 128,
+                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                               __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+        }
+        ub = (long long)sg.sk * a.nkb;
+        c0 = (int)(((ub + 1) * npairs - 1) / a.u_sk);
+        c1 = (int)(((ub + a.nkb) * npairs - 1) / a.u_sk);
+        __threadfence();
+        __syncwarp();
+        int prev = 0;
+        int* ctr = a.counters + sg.sk * 16 + rank * 8 + half * 4 + sub;
+        if (lane == 0) prev = atomicAdd(ctr, 1);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        finish = prev == c1 - c0;  // the last contributing pair reduces and writes the rows
+        if (finish) {
+          __threadfence();
+          if (lane == 0) *ctr = 0;
+        }
+      }
+      if (finish) {
+#pragma unroll 1
+        for (int c = half; c < BN / 32; c += 2) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + c * 32, r);
+          tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+#pragma unroll 1
+          for (int cc = c0; cc <= c1; ++cc) {
+            if (cc == pair) continue;
+            const long long cu0 = (long long)cc * a.u_sk / npairs;
+            const int slot = cu0 >= ub ? 0 : 1;
+            const float4* src = reinterpret_cast<const float4*>(a.partial) +
+                                (((size_t)(cc * 2 + slot) * 2 + rank) * (BN / 32) + c) * 8 * 128 +
+                                lrow;
+            float4 f[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = __ldcg(src + j * 128);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              v[4 * j] += f[j].x;
+              v[4 * j + 1] += f[j].y;
+              v[4 * j + 2] += f[j].z;
+              v[4 * j + 3] += f[j].w;
+            }
+          }
+          epi_chunk<EPI, false>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32, v, lane, 0u);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -866,7 +927,30 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     a.np = ceil_div(M, 256);
     a.nq = N / pair_bn;
     a.nkb = ceil_div(K, 64);
-    const int grid = 2 * std::min(a.np * a.nq, gemm_sms() / 2);
+    const int T = a.np * a.nq;
+    const int slots = gemm_sms() / 2;
+    // Stream-K over pairs for the last, partial wave (same schedule as the single-CTA
+    // kernel, per CTA half of the 256-row tile).  Opt-in (HY_PAIR_SK=1): measured on B200
+    // it does not pay for the serving shapes -- the fp32 partial round trip and the
+    // last-arriver fixup cost more than the idle pairs of the tail wave (e.g. 1600x4096x4096
+    // 69.8 us with, 54.8 us without; tools/kernel_sweep.py).
+    const size_t need = kCounterBytes + (size_t)slots * 2 * 2 * 128 * pair_bn * sizeof(float);
+    const double dp_eff = (double)T / ((double)ceil_div(T, slots) * slots);
+    bool sk = ws != nullptr && ws_bytes >= need && dp_eff < 0.9 && a.nkb >= 16 &&
+              getenv("HY_PAIR_SK") != nullptr;
+    int grid;
+    if (!sk) {
+      grid = 2 * std::min(T, slots);
+      a.t_dp = T;
+      a.u_sk = 0;
+    } else {
+      const int G = std::min(slots, T >= slots ? slots : 3 * T);
+      a.t_dp = T >= 2 * G ? (T / G - 1) * G : 0;
+      a.u_sk = (long long)(T - a.t_dp) * a.nkb;
+      a.counters = reinterpret_cast<int*>(ws);
+      a.partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + kCounterBytes);
+      grid = 2 * G;
+    }
     // The pair kernel does not release its dependents early: with an early trigger, a
     // PDL-launched pair GEMM plus early-launched dependents hung the serving replay on B200
     // (bisected with HY_PAIR_DBG: trigger off or PDL launch off both run clean).

@@ -84,6 +84,8 @@ def _gemm_ref(A, W, bias, act, res):
     (4096, 12288, 4096, 0, 0, False, False, False),    # heuristic picks the pair kernel
     (2816, 4096, 4096, 0, 0, False, True, False),      # heuristic: pair kernel, 128-wide tiles
     (700, 1408, 1024, 3, 4, False, False, False),      # forced pair, N % 256 != 0 -> BN 128
+    (3000, 4096, 4096, 3, 0, True, True, False),       # pair; + stream-K tail below
+    (3328, 4096, 11008, 0, 0, False, True, False),     # heuristic pair, down-proj shape
 ])
 def test_gemm(M, N, K, mode, act, bias, res, f32):
     g = torch.Generator(device=DEV).manual_seed(M * 7 + N)
@@ -100,6 +102,15 @@ def test_gemm(M, N, K, mode, act, bias, res, f32):
     ref = _gemm_ref(A, W, b, act, r)
     tol = 0.02 * max(1.0, ref.abs().max().item()) if not f32 else 2e-3 * max(1.0, ref.abs().max().item())
     assert (out.float() - ref).abs().max().item() <= tol
+
+
+@pytest.mark.parametrize("M,N,K,act", [(3000, 4096, 4096, 0), (600, 2048, 4096, 1),
+                                       (3328, 4096, 11008, 0)])
+def test_gemm_pair_stream_k(M, N, K, act, monkeypatch):
+    """Opt-in stream-K tail of the CTA-pair kernel (HY_PAIR_SK): partial tiles over pairs,
+    last-arriver fixup per CTA half, > 2 contributors per tile for small M."""
+    monkeypatch.setenv("HY_PAIR_SK", "1")
+    test_gemm(M, N, K, 3, act, act == 1, False, False)
 
 
 def test_gemm_row_map_and_inplace_residual():
