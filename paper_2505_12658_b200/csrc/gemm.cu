@@ -901,6 +901,8 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     HY_CHECK_ARG(false, "ldc must be a multiple of 8 for bf16 output");
   }
 
+  if (force_mode == 0)
+    if (const char* fm = getenv("HY_GEMM_MODE")) force_mode = atoi(fm);  // tuning only
   // CTA-pair kernel: large token counts, weight rows a multiple of 256
   // when it needs no more full waves than the single-CTA kernel (a pair tile takes about as
   // long on two SMs as a 128-row tile on one, so waves decide)

@@ -331,10 +331,10 @@ class InstanceRuntime:
         sv.wait_event(self.ev_start)
         self.sync_block_tables(sl)
         sampler = self.sampler
-        if sampler is not None:
-            sampler.before_batch()
         has_lang = bool(batch.decode_entries or batch.prefill_chunks)
         has_vis = bool(batch.encode_entries)
+        if sampler is not None:
+            sampler.before_batch(solo=not (has_lang and has_vis))
         out_rids: List[str] = []
         n_out = 0
         tok_off = 0

@@ -50,11 +50,17 @@ class KernelSampler:
         self.active = None
         # per class: list of (ms, work) per launch; plus sampled batch device time
         self.samples: Dict[str, List] = {k: [] for k in self.CLASSES}
+        # launches from batches where only one tower (one stream) ran: the kernel had the
+        # GPU to itself, so these durations are not inflated by the other stream's CTAs
+        self.solo_samples: Dict[str, List] = {k: [] for k in self.CLASSES}
+        self.solo = False
         self.batch_ms: Dict[str, float] = {k: 0.0 for k in self.CLASSES}
         self.class_ms: Dict[str, float] = {k: 0.0 for k in self.CLASSES}
         self.order = list(self.CLASSES)
 
-    def before_batch(self) -> None:
+    def before_batch(self, solo: bool = False) -> None:
+        """solo: only one tower runs in this batch (no cross-stream contention)."""
+        self.solo = solo
         self.n_batches += 1
         self.active = None
         if self.n_batches % self.every:
@@ -84,6 +90,8 @@ class KernelSampler:
             elif name == "vit_attn":
                 work = vit_attn_flops
             self.samples[name].append((ms, work))
+            if self.solo:
+                self.solo_samples[name].append((ms, work))
             tot += ms
             if name == "gemm" and self._shape[i]:
                 sh = self._shape[i]
@@ -112,8 +120,12 @@ class KernelSampler:
                 continue
             ms = sum(x for x, _ in s)
             work = sum(w for _, w in s)
+            so = self.solo_samples[name]
+            so_ms = sum(x for x, _ in so)
             out[name] = {"launches": len(s), "avg_ms": ms / len(s), "total_ms": ms,
                          "work": work, "work_per_ms": work / ms if ms > 0 else 0.0,
+                         "solo_launches": len(so),
+                         "solo_work_per_ms": sum(w for _, w in so) / so_ms if so_ms > 0 else 0.0,
                          "share_of_batch_time": (self.class_ms[name] / self.batch_ms[name]
                                                  if self.batch_ms[name] > 0 else 0.0)}
         return out
