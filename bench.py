@@ -298,8 +298,7 @@ def run_ours(args, d: Dist):
             ach = s["work_per_ms"] / 1e6  # bytes/ms -> GB/s
             return {"kernel": "attn_decode_kernel (K8)", "bound": "hbm", "achieved": ach,
                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
-                    "achieved_solo": s["solo_work_per_ms"] / 1e6,
-                    "solo_launches": s["solo_launches"],
+
                     "traffic": traffic_of("decode_attn"), "launches_timed": s["launches"],
                     "avg_launch_ms": s["avg_ms"], "share_of_step": s["share_of_batch_time"],
                     "peak_source": f"{peak_src} hbm_gbs"}
@@ -309,11 +308,7 @@ def run_ours(args, d: Dist):
                            "prefill_attn": "attn_tc_kernel<128,paged> (K7, tcgen05)",
                            "vit_attn": "attn_tc_kernel<64,varlen> (K3, tcgen05)"}[name],
                 "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
-                "frac": ach / pk,
-                # same class, launches from batches where only one tower ran (no CTAs of the
-                # other stream on the GPU); `achieved` above includes contended launches
-                "achieved_solo": s["solo_work_per_ms"] / 1e9, "solo_launches": s["solo_launches"],
-                "traffic": traffic_of(name), "launches_timed": s["launches"],
+                "frac": ach / pk, "traffic": traffic_of(name), "launches_timed": s["launches"],
                 "avg_launch_ms": s["avg_ms"], "share_of_step": s["share_of_batch_time"],
                 "peak_source": f"{peak_src} bf16_tflops_sustained"}
 

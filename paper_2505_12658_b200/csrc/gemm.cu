@@ -246,6 +246,10 @@ struct Seg {
 __device__ __forceinline__ int cta_segments(const GemmArgs& a, int c, int G, long long& u0,
                                             long long& u1) {
   const int n_dp = (a.t_dp - c + G - 1) / G;
+  if (a.u_sk == 0) {  // no stream-K: skip the 64-bit divisions
+    u0 = u1 = 0;
+    return n_dp;
+  }
   u0 = (long long)c * a.u_sk / G;
   u1 = (long long)(c + 1) * a.u_sk / G;
   const int n_sk = u1 > u0 ? (int)((u1 - 1) / a.nkb - u0 / a.nkb) + 1 : 0;
