@@ -355,6 +355,14 @@ def run_ours(args, d: Dist):
 
     # ---- KV-block migration copy (K10): block-granular gather/scatter of paged KV blocks
     mig = kv_migration_probe(dev, shape, peaks) if d.rank == 0 else None
+    if d.world > 1:
+        cross = kv_migration_cross_gpu(d, dev, shape, peaks)
+        if d.rank == 0 and mig is not None:
+            mig["cross_gpu"] = cross
+            if cross.get("p2p_gbs"):
+                mig["gbs"] = cross["p2p_gbs"]
+                mig["path"] = ("cross-GPU pull over NVLink: the destination GPU's copy kernel "
+                               "reads the source pool through a CUDA-IPC peer pointer")
 
     # ---- CPU baseline: the oracle port on the host cores (bounded sample)
     cpu = None
@@ -386,6 +394,125 @@ def run_ours(args, d: Dist):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line))
+
+
+def kv_migration_cross_gpu(d, dev, shape, peaks, n_blocks=128, reps=5):
+    """Prefill -> decode KV-block migration between GPUs (BASELINE config 5): ranks
+    pair up (2i -> 2i+1); every odd rank pulls n_blocks shuffled 8 MiB blocks from its even
+    partner, all pairs at once.  P2P: hy_copy_blocks on the destination GPU reading the
+    source pool through a CUDA-IPC peer pointer (one kernel, no staging).  Baseline: NCCL
+    send/recv of the same payload (gather to a contiguous buffer on the source, send, recv,
+    scatter on the destination).  Decisions are made collectively (gloo), so a failure on one
+    rank is reported, not deadlocked on."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2505_12658_b200 import _lib
+    out = {"pairs": d.world // 2, "blocks": n_blocks}
+    if d.world % 2:
+        return {"skipped": "odd world size"}
+    lib = _lib.load()
+    bb = shape.kv_block_elems * 2
+    src_side = d.rank % 2 == 0
+    partner = d.rank + 1 if src_side else d.rank - 1
+    pool = torch.empty(n_blocks * bb, dtype=torch.uint8, device=dev)
+    if src_side:
+        pool.random_(0, 255)
+    rng = np.random.default_rng(1)
+    sid = torch.from_numpy(rng.permutation(n_blocks).astype(np.int32)).to(dev)
+    did = torch.from_numpy(rng.permutation(n_blocks).astype(np.int32)).to(dev)
+    st = torch.cuda.current_stream(dev)
+    payload = n_blocks * bb
+
+    def ev_time(fn, sync=True):
+        fn()
+        st.synchronize()
+        ts = []
+        for _ in range(reps):
+            if sync:
+                d.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            fn()
+            b.record(st)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    torch.cuda.synchronize(dev)
+    d.barrier()  # source pools filled before anyone reads them
+    # ---- P2P pull through a CUDA-IPC handle of the partner's pool (timed on the puller
+    # alone; every rank reaches the one reduce below whatever happens)
+    ok, err = 1, ""
+    peer = None
+    mine = None
+    try:
+        mine = pool.untyped_storage()._share_cuda_() if src_side else None
+    except Exception as e:  # noqa: BLE001
+        ok, err = 0, f"ipc export: {type(e).__name__}: {e}"[:200]
+    handles = [None] * d.world
+    dist.all_gather_object(handles, mine)  # every rank, whatever happened above
+    try:
+        if not src_side:
+            if handles[partner] is None:
+                raise RuntimeError("partner exported no IPC handle")
+            peer = torch.UntypedStorage._new_shared_cuda(*handles[partner])
+    except Exception as e:  # noqa: BLE001
+        ok, err = 0, f"ipc open: {type(e).__name__}: {e}"[:200]
+    all_ok = int(d.reduce([ok])[0]) == d.world
+    if all_ok:
+        try:
+            t_p2p = 0.0
+            if not src_side:
+                def pull():
+                    _lib.check(lib.hy_copy_blocks(peer.data_ptr(), pool.data_ptr(),
+                                                  sid.data_ptr(), did.data_ptr(), n_blocks, bb,
+                                                  st.cuda_stream), "hy_copy_blocks(peer)")
+                t_p2p = ev_time(pull, sync=False)
+        except Exception as e:  # noqa: BLE001
+            t_p2p, out["p2p_error"] = 0.0, f"{type(e).__name__}: {e}"[:200]
+        try:
+            t_max = d.reduce([t_p2p], op="max")[0]
+            out["p2p_ms"] = t_max
+            out["p2p_gbs"] = payload / t_max / 1e6 if t_max > 0 else None
+            out["p2p_aggregate_gbs"] = out["p2p_gbs"] * (d.world // 2) if out["p2p_gbs"] else None
+        except Exception as e:  # noqa: BLE001
+            out["p2p_error"] = f"{type(e).__name__}: {e}"[:200]
+    else:
+        out["p2p_error"] = err or "ipc handle exchange failed on a rank"
+    # ---- NCCL send/recv baseline (same payload, contiguous staging)
+    try:
+        grp = dist.new_group(backend="nccl")
+        buf = torch.empty(payload, dtype=torch.uint8, device=dev)
+        seq = torch.arange(n_blocks, dtype=torch.int32, device=dev)
+
+        def nccl_once():
+            if src_side:
+                _lib.check(lib.hy_copy_blocks(pool.data_ptr(), buf.data_ptr(), sid.data_ptr(),
+                                              seq.data_ptr(), n_blocks, bb, st.cuda_stream),
+                           "gather")
+                dist.send(buf, dst=partner, group=grp)
+            else:
+                dist.recv(buf, src=partner, group=grp)
+                _lib.check(lib.hy_copy_blocks(buf.data_ptr(), pool.data_ptr(), seq.data_ptr(),
+                                              did.data_ptr(), n_blocks, bb, st.cuda_stream),
+                           "scatter")
+        t_n = ev_time(nccl_once)
+        t_max = d.reduce([t_n], op="max")[0]
+        out["nccl_ms"] = t_max
+        out["nccl_gbs"] = payload / t_max / 1e6
+        dist.destroy_process_group(grp)
+    except Exception as e:  # noqa: BLE001
+        out["nccl_error"] = f"{type(e).__name__}: {e}"[:200]
+    out["unit"] = "GB/s payload per pair (max time over ranks)"
+    out["link_peak_gbs"] = 770.0
+    if out.get("p2p_gbs"):
+        out["p2p_frac_of_link"] = out["p2p_gbs"] / 770.0
+    del pool, peer
+    torch.cuda.empty_cache()
+    if d.rank == 0:
+        log(f"cross-GPU migration: {out}")
+    return out
 
 
 def kv_migration_probe(dev, shape, peaks, n_blocks=256, reps=5):
