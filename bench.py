@@ -356,7 +356,10 @@ def run_ours(args, d: Dist):
     # ---- KV-block migration copy (K10): block-granular gather/scatter of paged KV blocks
     mig = kv_migration_probe(dev, shape, peaks) if d.rank == 0 else None
     if d.world > 1:
-        cross = kv_migration_cross_gpu(d, dev, shape, peaks)
+        try:
+            cross = kv_migration_cross_gpu(d, dev, shape, peaks)
+        except Exception as e:  # noqa: BLE001  (reported, never fatal to the bench line)
+            cross = {"error": f"{type(e).__name__}: {e}"[:200]}
         if d.rank == 0 and mig is not None:
             mig["cross_gpu"] = cross
             if cross.get("p2p_gbs"):
