@@ -914,12 +914,18 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   // (single-CTA 128x256 tiles: ~12% less efficient than a pair tile).
   bool pair = force_mode == 3;
   int pair_bn = 256;
+  int single_bn = 0;  // 0: default width for the single-CTA normal orientation
   if (force_mode == 0 && M >= kPairMinRows && N % 256 == 0 && !getenv("HY_GEMM_NOPAIR")) {
     const int sms = gemm_sms();
     const double t256 = ceil_div(ceil_div(M, 256) * (N / 256), sms / 2);
     const double t128 = 0.55 * ceil_div(ceil_div(M, 256) * (N / 128), sms / 2);
     const double t1 = 1.12 * ceil_div(ceil_div(M, 128) * (N / 256), sms);
-    pair = t256 <= t1;
+    // single-CTA 128x128 tiles: half the work of a 128x256 tile, less efficient per byte of
+    // shared memory; they win when the bigger tiles leave most SMs idle (ViT batches of a
+    // few images: M ~ 600-1800, N = 1024-3072)
+    const double t1n = 0.62 * ceil_div(ceil_div(M, 128) * (N / 128), sms);
+    pair = t256 <= std::min(t1, t1n);
+    if (!pair && t1n < t1 && !getenv("HY_GEMM_NO128")) single_bn = 128;
     // 128-wide pair tiles fill waves better on paper (t128) but measured slower inside the
     // serving sequence (tools/batch_bench.py: 2816-token prefill 42.2 vs 38.8 ms); they are
     // kept for N % 256 != 0 and HY_PAIR_BN=128 experiments
@@ -981,7 +987,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     a.P = N;
     a.Q = M;
   } else {
-    bn = (N % 256 == 0) ? 256 : 128;
+    bn = single_bn ? single_bn : (N % 256 == 0) ? 256 : 128;
     HY_CHECK_ARG(N % 128 == 0, "normal orientation needs N % 128 == 0");
     a.P = M;
     a.Q = N;
