@@ -243,21 +243,22 @@ struct Seg {
   int sk;        // stream-K tile index (tile - t_dp), or -1
 };
 
-__device__ __forceinline__ int cta_segments(const GemmArgs& a, int c, int G, long long& u0,
-                                            long long& u1) {
+// k-block unit ranges fit 32 bits (the host enables stream-K only when u_sk < 2^31), so
+// only the per-CTA range boundaries need one 64-bit product/division
+__device__ __forceinline__ int cta_segments(const GemmArgs& a, int c, int G, int& u0, int& u1) {
   const int n_dp = (a.t_dp - c + G - 1) / G;
   if (a.u_sk == 0) {  // no stream-K: skip the 64-bit divisions
     u0 = u1 = 0;
     return n_dp;
   }
-  u0 = (long long)c * a.u_sk / G;
-  u1 = (long long)(c + 1) * a.u_sk / G;
+  u0 = (int)((long long)c * a.u_sk / G);
+  u1 = (int)((long long)(c + 1) * a.u_sk / G);
   const int n_sk = u1 > u0 ? (int)((u1 - 1) / a.nkb - u0 / a.nkb) + 1 : 0;
   return n_dp + n_sk;
 }
 
-__device__ __forceinline__ Seg get_segment(const GemmArgs& a, int c, int G, int i, long long u0,
-                                           long long u1) {
+__device__ __forceinline__ Seg get_segment(const GemmArgs& a, int c, int G, int i, int u0,
+                                           int u1) {
   Seg s;
   const int n_dp = (a.t_dp - c + G - 1) / G;
   if (i < n_dp) {
@@ -269,8 +270,8 @@ __device__ __forceinline__ Seg get_segment(const GemmArgs& a, int c, int G, int 
     return s;
   }
   const int j = i - n_dp;
-  const long long t = u0 / a.nkb + j;
-  const long long lo = max(u0, t * a.nkb), hi = min(u1, (t + 1) * a.nkb);
+  const int t = u0 / a.nkb + j;
+  const int lo = max(u0, t * a.nkb), hi = min(u1, (t + 1) * a.nkb);
   s.tile = a.t_dp + (int)t;
   s.sk = (int)t;
   s.kb0 = (int)(lo - t * a.nkb);
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) HY_TR(1);
 
-  long long su0, su1;
+  int su0, su1;
   const int nseg = cta_segments(a, cta, G, su0, su1);
 
   if (warp == 0) {
@@ -599,7 +600,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  long long su0, su1;
+  int su0, su1;
   const int nseg = cta_segments(a, pair, npairs, su0, su1);  // data-parallel + stream-K
 
   if (warp == 0) {
@@ -949,7 +950,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     const size_t need = kCounterBytes + (size_t)slots * 2 * 2 * 128 * pair_bn * sizeof(float);
     const double dp_eff = (double)T / ((double)ceil_div(T, slots) * slots);
     bool sk = ws != nullptr && ws_bytes >= need && dp_eff < 0.9 && a.nkb >= 16 &&
-              getenv("HY_PAIR_SK") != nullptr;
+              (long long)T * a.nkb < (1LL << 31) && getenv("HY_PAIR_SK") != nullptr;
     int grid;
     if (!sk) {
       grid = 2 * std::min(T, slots);
@@ -1000,11 +1001,18 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   const int T = a.np * a.nq;
   const int sms = gemm_sms();
   const size_t need = kCounterBytes + (size_t)sms * 2 * 128 * bn * sizeof(float);
-  // stream-K only when whole-tile waves would leave the machine badly underfilled
+  // stream-K when whole-tile waves would leave SMs idle.  Swap orientation (decode: weight
+  // streaming, every SM must pull bytes): a mostly idle last wave (fill < 85%) or a single
+  // wave under half full; normal orientation only
+  // below 50% fill with a long K loop -- measured there, with K = 1024 or a >= 50% full wave
+  // the fp32 partial round trip costs more than the idle SMs (tools/kernel_sweep.py)
   const double dp_eff = (double)T / ((double)ceil_div(T, sms) * sms);
-  bool sk = ws != nullptr && ws_bytes >= need && dp_eff < 0.85 && a.nkb >= 4;
+  const bool units_fit = (long long)T * a.nkb < (1LL << 31);  // 32-bit segment math
+  bool sk = ws != nullptr && ws_bytes >= need && units_fit &&
+            (swap ? (a.nkb >= 4 && (T > sms ? dp_eff < 0.85 : dp_eff < 0.5))
+                  : (dp_eff < 0.5 && a.nkb >= 32));
   if (getenv("HY_GEMM_NOSK")) sk = false;
-  if (getenv("HY_GEMM_SK")) sk = ws != nullptr && ws_bytes >= need;
+  if (getenv("HY_GEMM_SK")) sk = ws != nullptr && ws_bytes >= need && units_fit;
   int grid;
   if (!sk) {
     grid = std::min(T, sms);
