@@ -924,7 +924,9 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     // single-CTA 128x128 tiles: half the work of a 128x256 tile, less efficient per byte of
     // shared memory; they win when the bigger tiles leave most SMs idle (ViT batches of a
     // few images: M ~ 600-1800, N = 1024-3072)
-    const double t1n = 0.62 * ceil_div(ceil_div(M, 128) * (N / 128), sms);
+    // (only for short K: with long K loops the 128x128 tile's shared-memory bandwidth per
+    // flop dominates -- 1600x4096x4096 measured 78 us on 128x128 vs 48 us on pair tiles)
+    const double t1n = K <= 2048 ? 0.62 * ceil_div(ceil_div(M, 128) * (N / 128), sms) : 1e30;
     pair = t256 <= std::min(t1, t1n);
     if (!pair && t1n < t1 && !getenv("HY_GEMM_NO128")) single_bn = 128;
     // 128-wide pair tiles fill waves better on paper (t128) but measured slower inside the
