@@ -86,10 +86,13 @@ struct TcAttnParams {
   int ld_o;
 };
 
-template <int D>
+template <int D, int T = 2>
 struct TcAttnCfg {
   static constexpr int BQ = 128, BK = 128;
-  static constexpr int TILES = 2;                 // query tiles per CTA (ping-pong)
+  // T = 2: two query tiles per CTA, 4 softmax warps each, ping-pong between the tiles.
+  // T = 1: one query tile, 8 softmax warps (two threads per row, 64 keys each), S double-
+  //        buffered over key tiles so Q K^T of tile j+1 runs under the softmax of tile j.
+  static constexpr int TILES = T;
   static constexpr int NC = D / 64;               // 64-wide d chunks (one 128B swizzle row)
   static constexpr int CHUNK = 128 * 128;         // bytes of one [128 rows][64 bf16] chunk
   static constexpr int Q_BYTES = NC * CHUNK;      // one query tile
@@ -99,14 +102,14 @@ struct TcAttnCfg {
   // TMEM columns: tile t owns S_t (fp32, 128 cols) at t * 128, overwritten in place by P_t
   // (bf16 pairs, first 64 cols), and O_t at 256 + t * 128
   static constexpr int TMEM_COLS = 512;
-  static constexpr int THREADS = 64 + TILES * 128;
+  static constexpr int THREADS = 64 + 256;
 };
 
-template <int D, bool PAGED>
-__global__ void __launch_bounds__(64 + 2 * 128, 1)
+template <int D, bool PAGED, int T>
+__global__ void __launch_bounds__(64 + 256, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                    const TcAttnParams p) {
-  using C = TcAttnCfg<D>;
+  using C = TcAttnCfg<D, T>;
   pdl_trigger();
   pdl_wait();  // Q (and for varlen K/V) are written by the previous kernel on the stream
   const int seq = blockIdx.x / p.q_tiles;
@@ -152,7 +155,7 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], T == 2 ? 4 : 8);
       mbar_init(&o_done[i], 1);
     }
     fence_mbar_init();
@@ -273,6 +276,7 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
       mbar_wait(q_full, 0);
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
+      if constexpr (T == 2) {
       issue_s(0, 0);
       issue_s(1, 0);
       umma_commit(&k_empty[0]);  // K_0 retired once both Q K^T complete
@@ -292,8 +296,46 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
         if (more) umma_commit(&k_empty[(j + 1) & 1]);
         umma_commit(&v_empty[j & 1]);  // V_j retired once both P V complete
       }
+      } else {
+        // one query tile: S(j) lives in TMEM buffer j & 1 (P(j) over it), O at column 256.
+        // S(j+1) is issued before P V(j), so it runs while the softmax works on S(j); it
+        // overwrites P(j-1), whose P V was issued (and executes) before it.
+        const uint32_t q_addr = smem_u32(sQ);
+        auto issue_s1 = [&](int j) {
+          const uint32_t k_addr = smem_u32(sKV + (j & 1) * C::STAGE_BYTES);
+#pragma unroll
+          for (int c = 0; c < C::NC; ++c)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_bf16(tmem + (j & 1) * 128, smem_desc_k_sw128(q_addr + c * C::CHUNK + k * 32),
+                        smem_desc_k_sw128(k_addr + c * C::CHUNK + k * 32), idesc_qk,
+                        (c | k) ? 1u : 0u);
+          umma_commit(&s_full[j & 1]);
+          umma_commit(&k_empty[j & 1]);
+        };
+        issue_s1(0);
+        for (int j = 0; j < n_kt; ++j) {
+          if (j + 1 < n_kt) {
+            mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+            tc_fence_after();
+            issue_s1(j + 1);
+          }
+          mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+          mbar_wait(&p_full[0], j & 1);
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(sKV + (j & 1) * C::STAGE_BYTES + C::KV_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < C::BK / 16; ++kk)
+            umma_bf16_ts(tmem + 256, tmem + (j & 1) * 128 + kk * 8,
+                         smem_desc_sw128(v_addr + kk * 2048, C::CHUNK, 1024), idesc_pv,
+                         (j > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(&o_done[0]);
+          umma_commit(&v_empty[j & 1]);
+        }
+      }
     }
   } else {
+    if constexpr (T == 2) {
     // ---------------- softmax: tile t = warps 2..5 / 6..9, one query row per thread -------
     const int t = (warp - 2) >> 2;
     const int sub = warp & 3;
@@ -411,6 +453,127 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
         }
       }
     }
+
+    } else {
+    // ---------------- softmax, one query tile: warps 2..9, two threads per row --------------
+    // warp w and w + 4 own the same 32 TMEM lanes (rows); the first takes keys [0, 64) of
+    // each key tile, the second [64, 128).  Row maxima are exchanged through shared memory
+    // (double-buffered by tile parity) with a 64-thread named barrier per row group.
+    __shared__ float xm[2][2][128];  // [tile parity][key half][row]
+    __shared__ float xl[2][128];
+    const int sub = warp & 3;
+    const int hc = (warp - 2) >> 2;  // key / O-column half
+    const int row = sub * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(sub * 32) << 16);
+    const uint32_t tO = tl + 256 + hc * (D / 2);
+    const int qrow = qbase + row;
+    const int qpos = off + qrow;
+    const int kmax = PAGED ? min(kv_len, qpos + 1) : kv_len;  // keys [0, kmax) are valid
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kt; ++j) {
+      const int b = j & 1;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      const int kbase = j * C::BK + hc * 64;
+      const bool full = __all_sync(0xffffffffu, kbase + 64 <= kmax);
+      uint32_t r[64];
+      tmem_ld_32x32b_x32(tl + b * 128 + hc * 64, r);
+      tmem_ld_32x32b_x32(tl + b * 128 + hc * 64 + 32, r + 32);
+      tmem_ld_wait();
+      float mx8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+      if (full) {
+#pragma unroll
+        for (int u = 0; u < 64; ++u) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
+      } else {
+#pragma unroll
+        for (int u = 0; u < 64; ++u)
+          if (kbase + u < kmax) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
+      }
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      xm[b][hc][row] = mx;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + sub) : "memory");
+      mx = fmaxf(mx, xm[b][hc ^ 1][row]);
+      mx = mx == -INFINITY ? mx : mx * p.scale_log2;
+      const float m_new = fmaxf(m_used, mx);
+      if (j >= 1) {
+        mbar_wait(&o_done[0], (j - 1) & 1);  // P V(j-1) retired: O stable
+        tc_fence_after();
+        const bool need = m_new > m_used + 8.f;
+        if (__any_sync(0xffffffffu, need)) {
+          const float f = !need ? 1.f : (m_used == -INFINITY ? 0.f : exp2f(m_used - m_new));
+          l *= f;
+          if (need) m_used = m_new;
+#pragma unroll 1
+          for (int c = 0; c < D / 64; ++c) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tO + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * f);
+            tmem_st_32x32b_x32(tO + c * 32, o);
+          }
+        }
+      } else {
+        m_used = m_new;
+      }
+      const float ms = m_used == -INFINITY ? 0.f : m_used;
+      uint64_t rs2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
+      const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2), nms2 = pk2(-ms, -ms);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int k0 = c * 32 + 2 * u;
+          float x0, x1;
+          up2(ffma2(pk2(__uint_as_float(r[k0]), __uint_as_float(r[k0 + 1])), sc2, nms2), x0, x1);
+          float e0 = ex2_approx(x0);
+          float e1 = ex2_approx(x1);
+          if (!full) {
+            e0 = kbase + k0 < kmax ? e0 : 0.f;
+            e1 = kbase + k0 + 1 < kmax ? e1 : 0.f;
+          }
+          rs2[u & 1] = fadd2(rs2[u & 1], pk2(e0, e1));
+          pk[u] = pack_bf16x2(e0, e1);
+        }
+        tmem_st_32x32b_x16(tl + b * 128 + hc * 32 + c * 16, pk);
+      }
+      float ra, rb, rc, rd;
+      up2(rs2[0], ra, rb);
+      up2(rs2[1], rc, rd);
+      l += (ra + rb) + (rc + rd);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[0]);
+    }
+    // O / (l_lo + l_hi) -> global, each thread its half of the head dims
+    xl[hc][row] = l;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + sub) : "memory");
+    const float lt = l + xl[hc ^ 1][row];
+    mbar_wait(&o_done[0], (n_kt - 1) & 1);
+    tc_fence_after();
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tO + c * 32, o);
+      tmem_ld_wait();
+      if (qrow < nq) {
+        bf16* dst = p.out + (size_t)(q0 + qrow) * p.ld_o + (size_t)h * D + hc * (D / 2) + c * 32;
+#pragma unroll
+        for (int u = 0; u < 32; u += 8) {
+          float v[8];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) v[w] = __uint_as_float(o[u + w]) * inv;
+          store_bf16x8(dst + u, v);
+        }
+      }
+    }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -420,20 +583,31 @@ __global__ void __launch_bounds__(64 + 2 * 128, 1)
   }
 }
 
-template <int D, bool PAGED>
+template <int D, bool PAGED, int T>
 static int launch_tc_attn(const CUtensorMap& tq, const CUtensorMap& tkv, const TcAttnParams& p,
                           int n_seqs, int n_heads, cudaStream_t st) {
-  using C = TcAttnCfg<D>;
+  using C = TcAttnCfg<D, T>;
   static bool attr = false;
   if (!attr) {
-    HY_CUDA_RET(cudaFuncSetAttribute(attn_tc_kernel<D, PAGED>,
+    HY_CUDA_RET(cudaFuncSetAttribute(attn_tc_kernel<D, PAGED, T>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  HY_CUDA_RET(launch_pdl(attn_tc_kernel<D, PAGED>, dim3(n_seqs * p.q_tiles, n_heads),
+  HY_CUDA_RET(launch_pdl(attn_tc_kernel<D, PAGED, T>, dim3(n_seqs * p.q_tiles, n_heads),
                          dim3(C::THREADS), C::SMEM, st, tq, tkv, p));
   HY_LAUNCH_CHECK();
   return 0;
+}
+
+// Query tiles per CTA.  Two (ping-pong between the tiles) measured fastest except when the
+// grid would not cover half the SMs (a single small image: 48 CTAs), where one tile per CTA
+// with two softmax threads per row doubles the CTAs (1-image ViT 15.5 -> 9.7 us; 2304-token
+// prefill 91 us with two tiles, 118 with one).  HY_ATTN_T=1/2 forces.
+static int attn_tiles(int n_seqs, int max_q, int n_heads) {
+  const char* e = getenv("HY_ATTN_T");
+  const int forced = e ? atoi(e) : 0;
+  if (forced == 1 || forced == 2) return forced;
+  return (long long)n_seqs * ceil_div(max_q, 256) * n_heads < 64 ? 1 : 2;
 }
 
 // Paged prefill: Q rows of the chunk batch [n_rows, ld_q]; K/V from the paged cache of one
@@ -450,7 +624,8 @@ int attn_tc_prefill(const void* q, int ld_q, int n_rows, int n_seqs, const int* 
   p.slots = slots;
   p.block_table = block_table;
   p.bt_stride = bt_stride;
-  p.q_tiles = ceil_div(max_q, 256);  // pairs of 128-row query tiles
+  const int T = attn_tiles(n_seqs, max_q, n_heads);
+  p.q_tiles = ceil_div(max_q, 128 * T);
   p.group = n_heads / n_kv_heads;
   p.rows_per_block = block_stride / head_dim;
   p.rows_per_kv = n_kv_heads * HY_KV_BLOCK_TOKENS;
@@ -463,8 +638,11 @@ int attn_tc_prefill(const void* q, int ld_q, int n_rows, int n_seqs, const int* 
   // the whole pool as rows of head_dim elements; rows addressed through the block table
   HY_RET_IF(make_tmap_2d_bf16(&tkv, kv_layer, (1ull << 31) - 1, head_dim, (uint64_t)head_dim * 2,
                               HY_KV_BLOCK_TOKENS, 64));
-  if (head_dim == 128) return launch_tc_attn<128, true>(tq, tkv, p, n_seqs, n_heads, st);
-  return launch_tc_attn<64, true>(tq, tkv, p, n_seqs, n_heads, st);
+  if (T == 2)
+    return head_dim == 128 ? launch_tc_attn<128, true, 2>(tq, tkv, p, n_seqs, n_heads, st)
+                           : launch_tc_attn<64, true, 2>(tq, tkv, p, n_seqs, n_heads, st);
+  return head_dim == 128 ? launch_tc_attn<128, true, 1>(tq, tkv, p, n_seqs, n_heads, st)
+                         : launch_tc_attn<64, true, 1>(tq, tkv, p, n_seqs, n_heads, st);
 }
 
 // Varlen (ViT): packed QKV rows [n_rows, ld_qkv] = [Q heads | K heads | V heads].
@@ -474,7 +652,8 @@ int attn_tc_varlen(const void* qkv, int ld_qkv, int n_rows, int n_segs, const in
   HY_CHECK_ARG(head_dim == 128 || head_dim == 64, "tcgen05 attention: head_dim 64 or 128");
   TcAttnParams p{};
   p.qstart = seg;
-  p.q_tiles = ceil_div(max_len, 256);
+  const int T = attn_tiles(n_segs, max_len, n_heads);
+  p.q_tiles = ceil_div(max_len, 128 * T);
   p.group = 1;
   p.k_col0 = n_heads * head_dim;
   p.v_col0 = 2 * n_heads * head_dim;
@@ -484,8 +663,11 @@ int attn_tc_varlen(const void* qkv, int ld_qkv, int n_rows, int n_segs, const in
   CUtensorMap tm;
   HY_RET_IF(make_tmap_2d_bf16(&tm, qkv, n_rows, (uint64_t)3 * n_heads * head_dim,
                               (uint64_t)ld_qkv * 2, 128, 64));
-  if (head_dim == 128) return launch_tc_attn<128, false>(tm, tm, p, n_segs, n_heads, st);
-  return launch_tc_attn<64, false>(tm, tm, p, n_segs, n_heads, st);
+  if (T == 2)
+    return head_dim == 128 ? launch_tc_attn<128, false, 2>(tm, tm, p, n_segs, n_heads, st)
+                           : launch_tc_attn<64, false, 2>(tm, tm, p, n_segs, n_heads, st);
+  return head_dim == 128 ? launch_tc_attn<128, false, 1>(tm, tm, p, n_segs, n_heads, st)
+                         : launch_tc_attn<64, false, 1>(tm, tm, p, n_segs, n_heads, st);
 }
 
 }  // namespace hy

@@ -215,7 +215,9 @@ def test_decode_attention(n_heads, n_kv, ctxs):
     (28, 4, [(576, 40), (0, 129)]),
     (8, 8, [(1000, 300), (0, 1), (127, 129)]),         # many KV tiles, 1-row chunk
 ])
-def test_prefill_attention_paged(n_heads, n_kv, chunks):
+@pytest.mark.parametrize("tiles", ["1", "2"])  # query tiles per CTA of the tcgen05 kernel
+def test_prefill_attention_paged(n_heads, n_kv, chunks, tiles, monkeypatch):
+    monkeypatch.setenv("HY_ATTN_T", tiles)
     d, L, layer = 128, 2, 0
     ctxs = [o + c for o, c in chunks]
     n = len(chunks)
@@ -244,9 +246,11 @@ def test_prefill_attention_paged(n_heads, n_kv, chunks):
         r0 += c
 
 
+@pytest.mark.parametrize("tiles", ["1", "2"])  # query tiles per CTA of the tcgen05 kernel
 @pytest.mark.parametrize("d,lens", [(64, [577, 577, 10]), (80, [1024, 64, 300]), (128, [65]),
                                     (128, [300, 129, 1])])
-def test_vit_varlen_attention(d, lens):
+def test_vit_varlen_attention(d, lens, tiles, monkeypatch):
+    monkeypatch.setenv("HY_ATTN_T", tiles)
     nh = 4
     T = sum(lens)
     qkv = torch.randn(T, 3 * nh * d, device=DEV).bfloat16()
