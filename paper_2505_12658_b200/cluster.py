@@ -36,6 +36,7 @@ from .executor import CLOCKS, InstanceRuntime
 from .inputs import ImageStore
 from .shapes import MllmShape
 from .weights import DeviceWeights
+from .wire import BlockMap, MigrationMessage
 
 
 class GpuMigrationJob(MG.MigrationJob):
@@ -183,6 +184,15 @@ class GpuCluster(C.Cluster):
         self.transfer_stats["seconds"] += ms * 1e-3
         self.migration_log.append((job.kind, job.source, job.target, job.rid,
                                    [(w, list(s), list(d)) for w, s, d, *_ in maps], ms))
+        # the control message a separate-process target would receive (wire.py, f4)
+        iids = list(self.instances)
+        msg = MigrationMessage(
+            job.kind, job.rid, iids.index(job.source), iids.index(job.target), r.kv_len,
+            -1, int(job.kv_bytes + job.image_bytes), self.seed,
+            tuple(BlockMap(w, bb, tuple(s), tuple(d)) for w, s, d, _, _, bb in maps))
+        self.transfer_stats["control_bytes"] = (self.transfer_stats.get("control_bytes", 0) +
+                                                len(msg.to_bytes()))
+        self.last_migration_message = msg
         if self.clock == "oracle":
             return MG.MigrationJob.transfer_seconds(job, hw)
         return ms * 1e-3

@@ -101,6 +101,13 @@ def test_tiny_cluster_parity(name):
     # every request produced exactly output_tokens tokens
     for rid, toks in cl.generated.items():
         assert len(toks) == cl.reqs[rid].spec.output_tokens
+    # the last migration's control message (wire.py) carries exactly the copied page tables
+    if cl.migration_log:
+        from paper_2505_12658_b200.wire import MigrationMessage
+        kind, src, dst, rid, maps, _ms = cl.migration_log[-1]
+        msg = MigrationMessage.from_bytes(cl.last_migration_message.to_bytes())
+        assert (msg.kind, msg.rid) == (kind, rid)
+        assert [(m.pool, list(m.src_ids), list(m.dst_ids)) for m in msg.maps] == maps
 
 
 def test_qwen_shaped_hybrid_ep_d_parity():
