@@ -47,9 +47,19 @@ __device__ __forceinline__ void trace(int i) {
     g_trace[16 + i] = clock64();
   }
 }
+// per-CTA marks: [cta][0] entry, [1] first full barrier, [2] last accumulator handed to the
+// epilogue, [3] exit
+__device__ unsigned long long g_ctr[160][4];
+__device__ __forceinline__ void cta_mark(int i) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  g_ctr[blockIdx.x][i] = t;
+}
 #define HY_TR(i) trace(i)
+#define HY_CM(i) cta_mark(i)
 #else
 #define HY_TR(i)
+#define HY_CM(i)
 #endif
 
 enum EpiKind : int { EPI_BF16 = 0, EPI_QGELU = 1, EPI_GELU = 2, EPI_SWIGLU = 4, EPI_F32 = 5 };
@@ -302,7 +312,10 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
   const int lane = threadIdx.x & 31;
   const int G = gridDim.x;
   const int cta = blockIdx.x;
-  if (threadIdx.x == 0) HY_TR(0);
+  if (threadIdx.x == 0) {
+    HY_TR(0);
+    HY_CM(0);
+  }
   pdl_trigger();  // all CTAs are resident from the start (persistent grid <= #SMs)
 
   if (warp == 0 && lane == 0) {
@@ -400,7 +413,10 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
-          if (kb == sg.kb0 && i == 0) HY_TR(4);
+          if (kb == sg.kb0 && i == 0) {
+            HY_TR(4);
+            HY_CM(1);
+          }
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
@@ -416,6 +432,7 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
         }
         umma_commit(&tfull[acc]);
         if (i == 0) HY_TR(5);
+        if (i == nseg - 1) HY_CM(2);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -528,7 +545,10 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
-    if (lane == 0) HY_TR(8);
+    if (lane == 0) {
+      HY_TR(8);
+      HY_CM(3);
+    }
   }
 }
 
@@ -833,7 +853,7 @@ static int launch_bn(int bn, const CUtensorMap& tA, const CUtensorMap& tB, const
                      int grid, cudaStream_t st) {
   switch (bn) {
     case 32: return SWAP ? launch_gemm<32, SWAP, EPI>(tA, tB, a, grid, st) : -1;
-    case 64: return SWAP ? launch_gemm<64, SWAP, EPI>(tA, tB, a, grid, st) : -1;
+    case 64: return launch_gemm<64, SWAP, EPI>(tA, tB, a, grid, st);
     case 128: return launch_gemm<128, SWAP, EPI>(tA, tB, a, grid, st);
     case 256: return launch_gemm<256, SWAP, EPI>(tA, tB, a, grid, st);
     default: return -1;
@@ -927,8 +947,11 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     // (only for short K: with long K loops the 128x128 tile's shared-memory bandwidth per
     // flop dominates -- 1600x4096x4096 measured 78 us on 128x128 vs 48 us on pair tiles)
     const double t1n = K <= 2048 ? 0.62 * ceil_div(ceil_div(M, 128) * (N / 128), sms) : 1e30;
-    pair = t256 <= std::min(t1, t1n);
-    if (!pair && t1n < t1 && !getenv("HY_GEMM_NO128")) single_bn = 128;
+    // 128x64 tiles for the smallest of these (one or two images: a handful of 128x128 tiles)
+    const double t1q = K <= 2048 && !getenv("HY_GEMM_NO64") ? 0.38 * ceil_div(ceil_div(M, 128) * (N / 64), sms) : 1e30;
+    pair = t256 <= std::min(std::min(t1, t1n), t1q);
+    if (!pair && std::min(t1n, t1q) < t1 && !getenv("HY_GEMM_NO128"))
+      single_bn = t1q < t1n ? 64 : 128;
     // 128-wide pair tiles fill waves better on paper (t128) but measured slower inside the
     // serving sequence (tools/batch_bench.py: 2816-token prefill 42.2 vs 38.8 ms); they are
     // kept for N % 256 != 0 and HY_PAIR_BN=128 experiments

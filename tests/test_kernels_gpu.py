@@ -71,6 +71,8 @@ def _gemm_ref(A, W, bias, act, res):
     (256, 32000, 512, 0, 0, False, False, True),      # lm_head fp32 logits
     (577, 3072, 1024, 0, 0, True, False, False),      # ViT QKV
     (1000, 4096, 1024, 0, 1, True, False, False),     # ViT FC1 QuickGELU
+    (577, 1024, 1024, 0, 0, True, True, False),       # ViT O + residual: 128x64 tiles
+    (640, 1536, 512, 0, 4, False, False, False),      # 128x64 tiles + SwiGLU pairing
     (1252, 2816, 512, 0, 4, False, False, False),     # prefill SwiGLU, normal mode
     (4096, 1024, 4096, 2, 0, True, True, False),
     (300, 512, 640, 0, 0, False, False, False),       # patch-embed K padding

@@ -31,7 +31,14 @@ int main(int argc, char** argv) {
   cudaMalloc(&ws, 64 << 20); cudaMemset(ws, 0, 64 << 20);
   cudaMemset(A, 0, 64 << 20); cudaMemset(W, 0, 256 << 20);
   int shapes[][3] = {{128, 128, 64}, {128, 128, 1024}, {256, 4096, 64}, {1024, 2048, 64}, {577, 1024, 1024}, {64, 4096, 4096}, {2304, 4096, 4096}};
-  for (auto& s : shapes) {
+  int ns = sizeof(shapes) / sizeof(shapes[0]);
+  if (argc > 1) {  // gemm_lab MxNxK ...
+    ns = 0;
+    for (int i = 1; i < argc && ns < 7; ++i, ++ns)
+      sscanf(argv[i], "%dx%dx%d", &shapes[ns][0], &shapes[ns][1], &shapes[ns][2]);
+  }
+  for (int si = 0; si < ns; ++si) {
+    int* s = shapes[si];
     int M = s[0], N = s[1], K = s[2];
     HyGemmEpilogue e{};
     e.out = C; e.ldc = N;
@@ -48,7 +55,29 @@ int main(int argc, char** argv) {
       cudaMemcpyFromSymbol(tr, hy::g_trace, sizeof(tr));
       printf("   trace:");
       for (int i = 1; i < 16; ++i) printf(" %d:%lld", i, (long long)(tr[i] - tr[0]));
-      printf("\n   MHz(0->8): %.0f  cycles 10->13: %lld 13->15: %lld\n", (double)(tr[24] - tr[16]) * 1e3 / (double)(tr[8] - tr[0]), (long long)(tr[29]-tr[26]), (long long)(tr[31]-tr[29]));
+      {
+        unsigned long long cm[160][4];
+        cudaMemcpyFromSymbol(cm, hy::g_ctr, sizeof(cm));
+        unsigned long long t0 = ~0ull, tfirst_max = 0, tend_max = 0, tmma_max = 0;
+        const int nc = 148;
+        for (int c = 0; c < nc; ++c) if (cm[c][0] && cm[c][0] < t0) t0 = cm[c][0];
+        printf("\n   per-CTA (ns from first entry): entry/first-full/last-mma/exit\n  ");
+        for (int c = 0; c < nc; ++c) {
+          if (!cm[c][0] || cm[c][0] < t0) continue;
+          if (cm[c][3] - t0 > 1000000000ull) continue;
+          if (c < 8 || c % 20 == 0)
+            printf(" [%d %lld/%lld/%lld/%lld]", c, (long long)(cm[c][0] - t0), (long long)(cm[c][1] - t0),
+                   (long long)(cm[c][2] - t0), (long long)(cm[c][3] - t0));
+          tfirst_max = std::max(tfirst_max, cm[c][1] - t0);
+          tmma_max = std::max(tmma_max, cm[c][2] - t0);
+          tend_max = std::max(tend_max, cm[c][3] - t0);
+        }
+        printf("\n   max first-full %lld  max last-mma %lld  max exit %lld\n", (long long)tfirst_max,
+               (long long)tmma_max, (long long)tend_max);
+        static unsigned long long zero[160][4];
+        cudaMemcpyToSymbol(hy::g_ctr, zero, sizeof(zero));
+      }
+      printf("   MHz(0->8): %.0f  cycles 10->13: %lld 13->15: %lld\n", (double)(tr[24] - tr[16]) * 1e3 / (double)(tr[8] - tr[0]), (long long)(tr[29]-tr[26]), (long long)(tr[31]-tr[29]));
 #endif
     }
   }
