@@ -27,6 +27,14 @@ int vit_gather_visual(const HyImageDesc* images, int n_images, int n_visual, int
 
 static constexpr size_t kGemmWs = 64ull << 20;  // split-K partials
 
+// Opt-in (HY_ATTN_FORK=1): measured on B200 (tools/mixed_batch.py, 64-256 decodes at ctx
+// 300-700 + 512-2816-token prefill chunks) the overlap is within +-2% of the serial order --
+// decode attention already fills every SM, so the prefill CTAs only fill its tail.
+static bool attn_fork_enabled() {
+  const char* e = getenv("HY_ATTN_FORK");
+  return e && e[0] == '1';
+}
+
 struct Carve {
   uint8_t* base;
   size_t off = 0;
@@ -126,6 +134,13 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
     HY_RET_IF(hy_rope_kv_append(w.qkv, qkv_cols, R, m->n_heads, m->n_kv_heads, D, b->pos,
                                 b->row_slot, kv->block_table, kv->bt_stride, kv_layer,
                                 kv->block_stride, m->rope_theta, st));
+    // decode attention (HBM-bound) and prefill attention (tensor-bound) read disjoint rows
+    // of qkv and write disjoint rows of attn: the prefill part runs on a side stream so the
+    // two can overlap
+    const bool fork = nd > 0 && b->n_prefill > 0 && np_rows > 0 && attn_fork_enabled();
+    cudaStream_t pst = st;
+    cudaEvent_t join = nullptr;
+    if (fork) HY_RET_IF(side_fork(st, &pst, &join));
     if (nd > 0) {
       timer_mark(HY_KCLASS_DECODE_ATTN, st, true, 0.0);
       HY_RET_IF(hy_attn_decode_paged(w.qkv, qkv_cols, nd, m->n_heads, m->n_kv_heads, D,
@@ -135,14 +150,15 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
       timer_mark(HY_KCLASS_DECODE_ATTN, st, false, 0.0);
     }
     if (b->n_prefill > 0 && np_rows > 0) {
-      timer_mark(HY_KCLASS_PREFILL_ATTN, st, true, 0.0);
+      timer_mark(HY_KCLASS_PREFILL_ATTN, pst, true, 0.0);
       HY_RET_IF(hy_attn_prefill_paged(w.qkv + (size_t)nd * qkv_cols, qkv_cols, np_rows, b->n_prefill,
                                       b->pf_qstart, b->pf_offset, b->pf_slot, b->pf_max_q,
                                       m->n_heads, m->n_kv_heads, D, kv->block_table,
                                       kv->bt_stride, kv_layer, kv->block_stride, scale,
-                                      w.attn + (size_t)nd * QD, QD, st));
-      timer_mark(HY_KCLASS_PREFILL_ATTN, st, false, 0.0);
+                                      w.attn + (size_t)nd * QD, QD, pst));
+      timer_mark(HY_KCLASS_PREFILL_ATTN, pst, false, 0.0);
     }
+    if (fork) HY_RET_IF(side_join(st, pst, join));
     HY_RET_IF(G(w.attn, QD, L.w_o, R, H, QD, nullptr, w.x, H, HY_ACT_NONE, w.x, H, 0));
     HY_RET_IF(rmsnorm(w.x, H, L.ffn_norm, w.t, H, R, H, m->rms_eps, nullptr, st));
     HY_RET_IF(G(w.t, H, L.w_gate_up, R, 2 * m->ffn, H, nullptr, nullptr, 0, HY_ACT_SWIGLU, w.f,

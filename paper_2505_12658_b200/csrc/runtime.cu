@@ -113,3 +113,50 @@ void timer_mark(int klass, cudaStream_t st, bool begin, double work, long long s
 }  // namespace hy
 
 extern "C" void hy_set_kernel_timer(HyKernelTimer* timer) { hy::g_timer = timer; }
+
+// ---------------------------------------------------------------------------
+// Side stream for independent work inside one forward (fork / join with events).  One per
+// host thread, device and stream priority: the forwards of a thread are stream-ordered on
+// their main stream, so one side stream and one event pair per thread suffice.
+// ---------------------------------------------------------------------------
+namespace hy {
+struct SideStream {
+  int dev = -1, prio = 0;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+int side_fork(cudaStream_t st, cudaStream_t* side, cudaEvent_t* join) {
+  thread_local SideStream cache[8];
+  int dev = 0, prio = 0;
+  HY_CUDA_RET(cudaGetDevice(&dev));
+  HY_CUDA_RET(cudaStreamGetPriority(st, &prio));
+  SideStream* e = nullptr;
+  for (auto& c : cache)
+    if (c.s && c.dev == dev && c.prio == prio) e = &c;
+  if (!e) {
+    for (auto& c : cache)
+      if (!c.s) {
+        e = &c;
+        break;
+      }
+    if (!e) return (int)cudaErrorNotSupported;
+    HY_CUDA_RET(cudaStreamCreateWithPriority(&e->s, cudaStreamNonBlocking, prio));
+    HY_CUDA_RET(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
+    HY_CUDA_RET(cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming));
+    e->dev = dev;
+    e->prio = prio;
+  }
+  HY_CUDA_RET(cudaEventRecord(e->fork, st));
+  HY_CUDA_RET(cudaStreamWaitEvent(e->s, e->fork, 0));
+  *side = e->s;
+  *join = e->join;
+  return 0;
+}
+
+int side_join(cudaStream_t st, cudaStream_t side, cudaEvent_t join) {
+  HY_CUDA_RET(cudaEventRecord(join, side));
+  HY_CUDA_RET(cudaStreamWaitEvent(st, join, 0));
+  return 0;
+}
+}  // namespace hy
