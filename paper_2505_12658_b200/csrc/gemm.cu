@@ -246,6 +246,37 @@ __device__ __forceinline__ void raster_tile(int t, const GemmArgs& a, int& p, in
   q = rr / gp;
 }
 
+// stream-K fixup: add up to 3 other contributors' fp32 partials of one 32-column chunk.
+// The first two contributors' loads are all issued before the first add so their L2 round
+// trips overlap (a plain loop serialises one round trip per contributor and chunk; three
+// in flight at once would spill under the 168-register cap).
+__device__ __forceinline__ void add_partials(float* v, const float4* const* srcs, int ns) {
+#pragma unroll 1
+  for (int s0 = 0; s0 < ns; s0 += 2) {
+    const bool two = s0 + 1 < ns;
+    float4 f[2][8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[0][j] = __ldcg(srcs[s0] + j * 128);
+    if (two)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[1][j] = __ldcg(srcs[s0 + 1] + j * 128);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 g = f[0][j];
+      if (two) {
+        g.x += f[1][j].x;
+        g.y += f[1][j].y;
+        g.z += f[1][j].z;
+        g.w += f[1][j].w;
+      }
+      v[4 * j] += g.x;
+      v[4 * j + 1] += g.y;
+      v[4 * j + 2] += g.z;
+      v[4 * j + 3] += g.w;
+    }
+  }
+}
+
 struct Seg {
   int tile;      // raster index
   int kb0, kb1;  // k-block range
@@ -511,19 +542,7 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
             srcs[ns++] = reinterpret_cast<const float4*>(a.partial) +
                          ((size_t)(cc * 2 + slot) * (BN / 32) + c) * 8 * 128 + lrow;
           }
-#pragma unroll 1
-          for (int s2 = 0; s2 < ns; ++s2) {
-            float4 f[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) f[j] = __ldcg(srcs[s2] + j * 128);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              v[4 * j] += f[j].x;
-              v[4 * j + 1] += f[j].y;
-              v[4 * j + 2] += f[j].z;
-              v[4 * j + 3] += f[j].w;
-            }
-          }
+          add_partials(v, srcs, ns);
           epi_chunk<EPI, SWAP>(a, p * 128 + sub * 32, q * BN + c * 32, v, lane,
                                smem_u32(stg_base) + (warp - 2) * kStgBytes);
           if (i == 0 && c == 0 && threadIdx.x == 64) HY_TR(11);
@@ -761,25 +780,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-#pragma unroll 1
-          for (int cc = c0; cc <= c1; ++cc) {
+          const float4* srcs[3];
+          int ns = 0;
+          for (int cc = c0; cc <= c1 && ns < 3; ++cc) {
             if (cc == pair) continue;
             const long long cu0 = (long long)cc * a.u_sk / npairs;
             const int slot = cu0 >= ub ? 0 : 1;
-            const float4* src = reinterpret_cast<const float4*>(a.partial) +
-                                (((size_t)(cc * 2 + slot) * 2 + rank) * (BN / 32) + c) * 8 * 128 +
-                                lrow;
-            float4 f[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) f[j] = __ldcg(src + j * 128);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              v[4 * j] += f[j].x;
-              v[4 * j + 1] += f[j].y;
-              v[4 * j + 2] += f[j].z;
-              v[4 * j + 3] += f[j].w;
-            }
+            srcs[ns++] = reinterpret_cast<const float4*>(a.partial) +
+                         (((size_t)(cc * 2 + slot) * 2 + rank) * (BN / 32) + c) * 8 * 128 + lrow;
           }
+          add_partials(v, srcs, ns);
           epi_chunk<EPI, false>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32, v, lane, 0u);
         }
       }
@@ -889,6 +899,12 @@ static int gemm_sms() {
 // token rows from which the CTA-pair kernel is used (tuned on B200, tools/kernel_sweep.py)
 static constexpr int kPairMinRows = 512;
 
+// Whole tiles before the stream-K part: all but the last 1-2 waves' worth, so every
+// stream-K share is >= one tile of k-blocks.  (Splitting only the remainder wave -- fewer
+// partial round trips, shares below a tile -- measured no better on B200: o/down
+// projections at M = 640-3600, tools/kernel_sweep.py.)
+static int sk_dp_tiles(int T, int G) { return T >= 2 * G ? (T / G - 1) * G : 0; }
+
 int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K,
               const HyGemmEpilogue* e, void* ws, size_t ws_bytes, cudaStream_t st, int force_mode) {
   HY_CHECK_ARG(M >= 0 && N > 0 && K > 0, "gemm shape");
@@ -983,7 +999,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
       a.u_sk = 0;
     } else {
       const int G = std::min(slots, T >= slots ? slots : 3 * T);
-      a.t_dp = T >= 2 * G ? (T / G - 1) * G : 0;
+      a.t_dp = sk_dp_tiles(T, G);
       a.u_sk = (long long)(T - a.t_dp) * a.nkb;
       a.counters = reinterpret_cast<int*>(ws);
       a.partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + kCounterBytes);
@@ -1047,7 +1063,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     const long long U = (long long)T * a.nkb;
     // at most 4 contributors per stream-K tile (T < sms: grid <= 3T)
     grid = (int)std::min<long long>(std::min<long long>(sms, U), T >= sms ? sms : 3LL * T);
-    a.t_dp = T >= 2 * grid ? (T / grid - 1) * grid : 0;
+    a.t_dp = sk_dp_tiles(T, grid);
     a.u_sk = (long long)(T - a.t_dp) * a.nkb;
     a.counters = reinterpret_cast<int*>(ws);
     a.partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + kCounterBytes);
