@@ -110,7 +110,6 @@ __global__ void __launch_bounds__(64 + 256, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                    const TcAttnParams p) {
   using C = TcAttnCfg<D, T>;
-  pdl_trigger();
   pdl_wait();  // Q (and for varlen K/V) are written by the previous kernel on the stream
   const int seq = blockIdx.x / p.q_tiles;
   // pair of 128-row query tiles, last pair first: under the causal mask later pairs see more
@@ -165,6 +164,7 @@ __global__ void __launch_bounds__(64 + 256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();  // only once this CTA holds its TMEM (see gemm_tc_kernel)
 
   if (warp == 0) {
     // ---------------- TMA producer (lane 0 issues; the warp fetches block-table entries) --

@@ -347,7 +347,6 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
     HY_TR(0);
     HY_CM(0);
   }
-  pdl_trigger();  // all CTAs are resident from the start (persistent grid <= #SMs)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -368,6 +367,11 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) HY_TR(1);
+  // Release dependents only once this CTA holds its tensor memory.  A dependent grid
+  // allocates TMEM before its griddepcontrol.wait; if it could start while a CTA of this
+  // grid had not allocated yet, the two would wait on each other (this grid's CTA for the
+  // columns, the dependent for this grid's completion).
+  pdl_trigger();
 
   int su0, su1;
   const int nseg = cta_segments(a, cta, G, su0, su1);
@@ -619,7 +623,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
-  if (!(a.dbg & 1)) pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -639,6 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (!(a.dbg & 1)) pdl_trigger();  // after both CTAs hold their TMEM: see gemm_tc_kernel
   int su0, su1;
   const int nseg = cta_segments(a, pair, npairs, su0, su1);  // data-parallel + stream-K
 
@@ -1005,10 +1009,9 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
       a.partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + kCounterBytes);
       grid = 2 * G;
     }
-    // The pair kernel does not release its dependents early: with an early trigger, a
-    // PDL-launched pair GEMM plus early-launched dependents hung the serving replay on B200
-    // (bisected with HY_PAIR_DBG: trigger off or PDL launch off both run clean).
-    a.dbg = 1;
+    // HY_PAIR_DBG=1: no early release of dependents (bisection aid; the serving hang it
+    // isolated was a trigger issued before the TMEM allocation, see gemm_tc_kernel)
+    a.dbg = 0;
     if (const char* d = getenv("HY_PAIR_DBG")) a.dbg = atoi(d);
     if (const char* g = getenv("HY_GEMM_GROUP")) a.group = atoi(g);
     CUtensorMap tA, tB;

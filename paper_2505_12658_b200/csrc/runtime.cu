@@ -12,11 +12,15 @@ static std::atomic<long long> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-// Programmatic dependent launch is OFF by default (HY_PDL=1 enables it).  With PDL on, the
-// two-stream serving replay (vision stream at high priority, or the CTA-pair GEMM releasing
-// its dependents early) hung on B200 within minutes; with it off, no hang was seen in any
-// run.  The kernels keep their griddepcontrol points, which are no-ops without the launch
-// attribute.  Cost: the next kernel's prologue no longer overlaps the previous kernel's tail.
+// Programmatic dependent launch is OFF by default (HY_PDL=1 enables it).  The hang PDL once
+// caused in the two-stream serving replay was a TMEM deadlock: the tcgen05 kernels released
+// their dependents before allocating tensor memory, so a dependent GEMM could take an SM's
+// columns and then wait for a primary CTA that was blocked allocating them.  Every TMEM
+// kernel now triggers only after its allocation (no hang in 3 replays + the GPU suite with
+// HY_PDL=1), but PDL measured ~2% SLOWER on the serving replay (device time 7.06-7.12 s vs
+// 6.95 s, tools/profile_serving.py --requests 400 --rate 90): early-launched dependents sit
+// on SMs the other stream could use.  The kernels keep their griddepcontrol points (no-ops
+// without the launch attribute).
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("HY_PDL");
