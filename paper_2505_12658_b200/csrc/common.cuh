@@ -116,6 +116,11 @@ __device__ __forceinline__ void sts_f32x4(uint32_t a, float x, float y, float z,
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w)
                : "memory");
 }
+__device__ __forceinline__ void sts_u32x4(uint32_t a, uint4 u) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(u.x), "r"(u.y), "r"(u.z),
+               "r"(u.w)
+               : "memory");
+}
 __device__ __forceinline__ float4 lds_f32x4(uint32_t a) {
   float4 r;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -201,6 +206,17 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* tm, uint64_t* bar
 }
 
 // Prefetch a 2D TMA box into L2 (no shared-memory destination, no completion tracking).
+// TMA store shared -> global (bulk-group completion) and its group waits
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+               ::"l"(tm), "r"(src), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* tm, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(tm),
                "r"(c0), "r"(c1)
@@ -408,8 +424,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
 // ---------------------------------------------------------------------------
 // host: TMA descriptor encoding through the driver entry point (no -lcuda)
 // ---------------------------------------------------------------------------
+// swizzle: CUtensorMapSwizzle (default 128B: the K-major MMA operand layout; 0 = none, for
+// the epilogue's row-major TMA stores)
 int make_tmap_2d_bf16(CUtensorMap* tm, const void* base, uint64_t rows, uint64_t cols,
-                      uint64_t row_stride_bytes, uint32_t box_rows, uint32_t box_cols);
+                      uint64_t row_stride_bytes, uint32_t box_rows, uint32_t box_cols,
+                      int swizzle = 3);
 
 int num_sms();
 

@@ -48,18 +48,22 @@ __device__ __forceinline__ void trace(int i) {
   }
 }
 // per-CTA marks: [cta][0] entry, [1] first full barrier, [2] last accumulator handed to the
-// epilogue, [3] exit
-__device__ unsigned long long g_ctr[160][4];
+// epilogue, [3] exit, [4] segments, [5] stream-K tiles finished by this CTA
+__device__ unsigned long long g_ctr[160][6];
 __device__ __forceinline__ void cta_mark(int i) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   g_ctr[blockIdx.x][i] = t;
 }
+#define HY_CNT(i, v) (g_ctr[blockIdx.x][i] = (v))
+#define HY_CINC(i) atomicAdd(&g_ctr[blockIdx.x][i], 1ull)
 #define HY_TR(i) trace(i)
 #define HY_CM(i) cta_mark(i)
 #else
 #define HY_TR(i)
 #define HY_CM(i)
+#define HY_CNT(i, v)
+#define HY_CINC(i)
 #endif
 
 enum EpiKind : int { EPI_BF16 = 0, EPI_QGELU = 1, EPI_GELU = 2, EPI_SWIGLU = 4, EPI_F32 = 5 };
@@ -68,7 +72,7 @@ struct GemmArgs {
   int P, Q, K;    // MMA-M extent (rows of map A), MMA-N extent (rows of map B), reduction
   int np, nq, nkb;
   int t_dp;       // whole tiles [0, t_dp) round-robin (multiple of the grid when stream-K)
-  int dbg;        // pair kernel PDL bits (HY_PAIR_DBG): 1 no early trigger, 2 no PDL launch
+  int dbg;        // bits: 1 no early PDL trigger, 2 no PDL launch (pair, HY_PAIR_DBG); 4 no residual prefetch
   int group;      // raster group of token tiles (0 = auto; HY_GEMM_GROUP tuning only)
   long long u_sk; // k-block units of tiles [t_dp, T), split evenly over the grid
   int M, N;       // logical GEMM shape (tokens, physical weight rows)
@@ -80,6 +84,7 @@ struct GemmArgs {
   int ldc;
   float* partial;  // [G][2][128][BN] fp32: first / last stream-K segment of each CTA
   int* counters;   // [tiles][8] arrival counters per stream-K tile and epilogue warp (zeroed)
+  int tma_out;     // normal orientation: bf16 output tiles leave through TMA stores (map tmC)
 };
 
 template <int EPI>
@@ -101,11 +106,14 @@ __device__ __forceinline__ float act_of(float x) {
 // rounding to bf16.
 constexpr int kEpiWarps = 8;             // two per TMEM lane sub-partition (even / odd chunks)
 constexpr int kStgStride = 32 * 4 + 16;  // bytes per staged row (pad: conflict-free 16B access)
-constexpr int kStgBytes = 16 * kStgStride;  // per epilogue warp: 16 token rows per pass
+// per epilogue warp: the swap orientation's fp32 staging (16 token rows x kStgStride per pass)
+// or, in the normal orientation, two 32 x 32 bf16 buffers for the TMA-store epilogue
+constexpr int kStgBytes = 4096;
+static_assert(16 * kStgStride <= kStgBytes, "swap staging");
 
 template <int EPI, bool SWAP>
 __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int p0, int q0, float* v, int lane,
-                                          uint32_t stg) {
+                                          uint32_t stg, const CUtensorMap* tmC, int& nst) {
   constexpr int OC = EPI == EPI_SWIGLU ? 16 : 32;  // output columns of this chunk
   int row0, col0;  // first output row (token), first output column
   if (!SWAP) {
@@ -128,10 +136,45 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int p0, int q0, flo
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = act_of<EPI>(v[j]);
     }
-    // direct row stores: each lane already owns OC contiguous outputs of one row (measured
-    // faster than staging for this orientation: the chunk latency is the limiter, not sectors)
+    // direct row stores (fp32 logits, row-mapped outputs): each lane owns OC contiguous
+    // outputs of one row
     const int m = p0 + lane;
     col0 = EPI == EPI_SWIGLU ? q0 / 2 : q0;
+    if (EPI != EPI_F32 && a.tma_out) {
+      // TMA-store epilogue: the warp's 32 rows x OC bf16 go through one of two shared
+      // buffers and leave as one bulk tensor store (full row segments, asynchronous), instead
+      // of 32 scattered 16-byte pieces per store instruction.  Rows >= M are clipped by TMA.
+      const uint32_t buf = stg + (nst & 1) * (kStgBytes / 2);
+      if (lane == 0) bulk_wait_read<1>();  // this buffer's store (two chunks ago) has read it
+      __syncwarp();
+      if (m < a.M && a.residual) {
+        const bf16* r = a.residual + (size_t)m * a.ldr + col0;
+#pragma unroll
+        for (int j = 0; j < OC; j += 8) {
+          float b[8];
+          load_bf16x8(r + j, b);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) v[j + t] += b[t];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < OC; j += 8) {
+        uint4 u;
+        u.x = pack_bf16x2(v[j], v[j + 1]);
+        u.y = pack_bf16x2(v[j + 2], v[j + 3]);
+        u.z = pack_bf16x2(v[j + 4], v[j + 5]);
+        u.w = pack_bf16x2(v[j + 6], v[j + 7]);
+        sts_u32x4(buf + lane * (OC * 2) + j * 2, u);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmC, buf, col0, p0);
+        bulk_commit();
+      }
+      ++nst;
+      return;
+    }
     if (m < a.M) {
       if (a.residual) {
         const bf16* r = a.residual + (size_t)m * a.ldr + col0;
@@ -246,6 +289,22 @@ __device__ __forceinline__ void raster_tile(int t, const GemmArgs& a, int& p, in
   q = rr / gp;
 }
 
+// Normal orientation: pull this thread's residual row segments of a tile into L2 while the
+// tile's MMAs are still running, so the epilogue's residual loads do not add a DRAM round
+// trip per 32-column chunk (the o / down projections add the residual stream in place).
+template <int BN, int EPI>
+__device__ __forceinline__ void prefetch_residual(const GemmArgs& a, int m, int qcol, int half) {
+  if (!a.residual || m >= a.M || (a.dbg & 4)) return;
+  const bf16* r = a.residual + (size_t)m * a.ldr;
+#pragma unroll
+  for (int c = half; c < BN / 32; c += 2) {
+    const int q0 = qcol + c * 32;
+    if (q0 >= a.N) break;
+    const int col0 = EPI == EPI_SWIGLU ? q0 / 2 : q0;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(r + col0));
+  }
+}
+
 // stream-K fixup: add up to 3 other contributors' fp32 partials of one 32-column chunk.
 // The first two contributors' loads are all issued before the first add so their L2 round
 // trips overlap (a plain loop serialises one round trip per contributor and chunk; three
@@ -324,7 +383,7 @@ __device__ __forceinline__ Seg get_segment(const GemmArgs& a, int c, int G, int 
 template <int BN, bool SWAP, int EPI>
 __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const GemmArgs a) {
+                   const __grid_constant__ CUtensorMap tmC, const GemmArgs a) {
   using C = GemmCfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -479,12 +538,14 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
     pdl_wait();  // residuals, partials and counters are written by earlier kernels
     const int sub = warp & 3;          // TMEM lane sub-partition this warp may access
     const int half = (warp - 2) >> 2;  // 32-column chunks half, half + 2, ...
+    int nst = 0;                       // TMA-store buffer toggle (normal orientation)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int i = 0; i < nseg; ++i) {
       const Seg sg = get_segment(a, cta, G, i, su0, su1);
       int p, q;
       raster_tile(sg.tile, a, p, q);
+      if (!SWAP && sg.slot < 0) prefetch_residual<BN, EPI>(a, p * 128 + sub * 32 + lane, q * BN, half);
       mbar_wait_sleepy(&tfull[acc], acc_phase);
       if (i == 0 && threadIdx.x == 64) HY_TR(6);
       tc_fence_after();
@@ -548,7 +609,7 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
           }
           add_partials(v, srcs, ns);
           epi_chunk<EPI, SWAP>(a, p * 128 + sub * 32, q * BN + c * 32, v, lane,
-                               smem_u32(stg_base) + (warp - 2) * kStgBytes);
+                               smem_u32(stg_base) + (warp - 2) * kStgBytes, &tmC, nst);
           if (i == 0 && c == 0 && threadIdx.x == 64) HY_TR(11);
           if (i == 0 && c == 1 && threadIdx.x == 64) HY_TR(12);
         }
@@ -562,6 +623,7 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_read<0>();  // TMA stores done reading shared memory
   }
   tc_fence_before();
   __syncthreads();
@@ -597,21 +659,23 @@ struct GemmPairCfg {
   static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM_BYTES =
+      STAGES * STAGE_BYTES + kEpiWarps * kStgBytes + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int THREADS = 64 + 32 * kEpiWarps;
 };
 
 template <int BN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const GemmArgs a) {
+                     const __grid_constant__ CUtensorMap tmC, const GemmArgs a) {
   using C = GemmPairCfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* stg_base = smem + C::STAGES * C::STAGE_BYTES;  // epilogue TMA-store buffers
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + kEpiWarps * kStgBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
@@ -623,6 +687,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
+  if (threadIdx.x == 0) HY_CM(0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -705,6 +770,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (i == 0 && kb == sg.kb0) HY_CM(1);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
@@ -720,6 +786,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
           }
         }
         umma_commit_cg2(&tfull[acc], 0x3);
+        if (i == nseg - 1) {
+          HY_CM(2);
+          HY_CNT(4, nseg);
+        }
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -732,12 +802,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
     const int sub = warp & 3;
     const int half = (warp - 2) >> 2;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    int nst = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int i = 0; i < nseg; ++i) {
       const Seg sg = get_segment(a, pair, npairs, i, su0, su1);
       int p, q;
       raster_tile(sg.tile, a, p, q);
+      if (sg.slot < 0) prefetch_residual<BN, EPI>(a, p * 256 + rank * 128 + sub * 32 + lane, q * BN, half);
       mbar_wait_sleepy(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN;
@@ -770,6 +842,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
         if (lane == 0) prev = atomicAdd(ctr, 1);
         prev = __shfl_sync(0xffffffffu, prev, 0);
         finish = prev == c1 - c0;  // the last contributing pair reduces and writes the rows
+        if (finish && lane == 0 && sub == 0 && half == 0) HY_CINC(5);
         if (finish) {
           __threadfence();
           if (lane == 0) *ctr = 0;
@@ -794,7 +867,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
                          (((size_t)(cc * 2 + slot) * 2 + rank) * (BN / 32) + c) * 8 * 128 + lrow;
           }
           add_partials(v, srcs, ns);
-          epi_chunk<EPI, false>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32, v, lane, 0u);
+          epi_chunk<EPI, false>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32, v, lane,
+                                smem_u32(stg_base) + (warp - 2) * kStgBytes, &tmC, nst);
         }
       }
       tc_fence_before();
@@ -805,6 +879,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_read<0>();  // TMA stores done reading shared memory
   }
   tc_fence_before();
   __syncthreads();
@@ -812,12 +887,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_cg2(tmem_base, C::TMEM_COLS);
+    if (lane == 0) HY_CM(3);
   }
 }
 
 template <int BN, int EPI>
-static int launch_pair(const CUtensorMap& tA, const CUtensorMap& tB, const GemmArgs& a, int grid,
-                       cudaStream_t st) {
+static int launch_pair(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
+                       const GemmArgs& a, int grid, cudaStream_t st) {
   using C = GemmPairCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -826,30 +902,30 @@ static int launch_pair(const CUtensorMap& tA, const CUtensorMap& tB, const GemmA
     attr_set = true;
   }
   if (a.dbg & 2)
-    gemm_pair_kernel<BN, EPI><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tA, tB, a);
+    gemm_pair_kernel<BN, EPI><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tA, tB, tC, a);
   else
     HY_CUDA_RET(launch_pdl(gemm_pair_kernel<BN, EPI>, dim3(grid), dim3(C::THREADS),
-                           C::SMEM_BYTES, st, tA, tB, a));
+                           C::SMEM_BYTES, st, tA, tB, tC, a));
   HY_LAUNCH_CHECK();
   return 0;
 }
 
 template <int BN>
 static int launch_pair_epi(int epi, const CUtensorMap& tA, const CUtensorMap& tB,
-                           const GemmArgs& a, int grid, cudaStream_t st) {
+                           const CUtensorMap& tC, const GemmArgs& a, int grid, cudaStream_t st) {
   switch (epi) {
-    case EPI_BF16: return launch_pair<BN, EPI_BF16>(tA, tB, a, grid, st);
-    case EPI_QGELU: return launch_pair<BN, EPI_QGELU>(tA, tB, a, grid, st);
-    case EPI_GELU: return launch_pair<BN, EPI_GELU>(tA, tB, a, grid, st);
-    case EPI_SWIGLU: return launch_pair<BN, EPI_SWIGLU>(tA, tB, a, grid, st);
-    case EPI_F32: return launch_pair<BN, EPI_F32>(tA, tB, a, grid, st);
+    case EPI_BF16: return launch_pair<BN, EPI_BF16>(tA, tB, tC, a, grid, st);
+    case EPI_QGELU: return launch_pair<BN, EPI_QGELU>(tA, tB, tC, a, grid, st);
+    case EPI_GELU: return launch_pair<BN, EPI_GELU>(tA, tB, tC, a, grid, st);
+    case EPI_SWIGLU: return launch_pair<BN, EPI_SWIGLU>(tA, tB, tC, a, grid, st);
+    case EPI_F32: return launch_pair<BN, EPI_F32>(tA, tB, tC, a, grid, st);
     default: return -1;
   }
 }
 
 template <int BN, bool SWAP, int EPI>
-static int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const GemmArgs& a, int grid,
-                       cudaStream_t st) {
+static int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
+                       const GemmArgs& a, int grid, cudaStream_t st) {
   using C = GemmCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -857,32 +933,33 @@ static int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const GemmA
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
     attr_set = true;
   }
-  HY_CUDA_RET(launch_pdl(gemm_tc_kernel<BN, SWAP, EPI>, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES, st, tA, tB, a));
+  HY_CUDA_RET(launch_pdl(gemm_tc_kernel<BN, SWAP, EPI>, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES,
+                         st, tA, tB, tC, a));
   HY_LAUNCH_CHECK();
   return 0;
 }
 
 template <bool SWAP, int EPI>
-static int launch_bn(int bn, const CUtensorMap& tA, const CUtensorMap& tB, const GemmArgs& a,
-                     int grid, cudaStream_t st) {
+static int launch_bn(int bn, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
+                     const GemmArgs& a, int grid, cudaStream_t st) {
   switch (bn) {
-    case 32: return SWAP ? launch_gemm<32, SWAP, EPI>(tA, tB, a, grid, st) : -1;
-    case 64: return launch_gemm<64, SWAP, EPI>(tA, tB, a, grid, st);
-    case 128: return launch_gemm<128, SWAP, EPI>(tA, tB, a, grid, st);
-    case 256: return launch_gemm<256, SWAP, EPI>(tA, tB, a, grid, st);
+    case 32: return SWAP ? launch_gemm<32, SWAP, EPI>(tA, tB, tC, a, grid, st) : -1;
+    case 64: return launch_gemm<64, SWAP, EPI>(tA, tB, tC, a, grid, st);
+    case 128: return launch_gemm<128, SWAP, EPI>(tA, tB, tC, a, grid, st);
+    case 256: return launch_gemm<256, SWAP, EPI>(tA, tB, tC, a, grid, st);
     default: return -1;
   }
 }
 
 template <bool SWAP>
 static int launch_epi(int epi, int bn, const CUtensorMap& tA, const CUtensorMap& tB,
-                      const GemmArgs& a, int grid, cudaStream_t st) {
+                      const CUtensorMap& tC, const GemmArgs& a, int grid, cudaStream_t st) {
   switch (epi) {
-    case EPI_BF16: return launch_bn<SWAP, EPI_BF16>(bn, tA, tB, a, grid, st);
-    case EPI_QGELU: return launch_bn<SWAP, EPI_QGELU>(bn, tA, tB, a, grid, st);
-    case EPI_GELU: return launch_bn<SWAP, EPI_GELU>(bn, tA, tB, a, grid, st);
-    case EPI_SWIGLU: return launch_bn<SWAP, EPI_SWIGLU>(bn, tA, tB, a, grid, st);
-    case EPI_F32: return launch_bn<SWAP, EPI_F32>(bn, tA, tB, a, grid, st);
+    case EPI_BF16: return launch_bn<SWAP, EPI_BF16>(bn, tA, tB, tC, a, grid, st);
+    case EPI_QGELU: return launch_bn<SWAP, EPI_QGELU>(bn, tA, tB, tC, a, grid, st);
+    case EPI_GELU: return launch_bn<SWAP, EPI_GELU>(bn, tA, tB, tC, a, grid, st);
+    case EPI_SWIGLU: return launch_bn<SWAP, EPI_SWIGLU>(bn, tA, tB, tC, a, grid, st);
+    case EPI_F32: return launch_bn<SWAP, EPI_F32>(bn, tA, tB, tC, a, grid, st);
     default: return -1;
   }
 }
@@ -902,6 +979,20 @@ static int gemm_sms() {
 }
 // token rows from which the CTA-pair kernel is used (tuned on B200, tools/kernel_sweep.py)
 static constexpr int kPairMinRows = 512;
+
+// Output map for the normal orientation's TMA-store epilogue: bf16 output without a row
+// map, 16B-aligned base (ldc % 8 == 0 is checked by the caller); box 32 rows x 32 outputs
+// (16 for SwiGLU, whose chunks emit half their columns).  Otherwise a.tma_out stays 0 and
+// the epilogue stores rows directly.  HY_GEMM_NOTMASTORE=1 forces the direct stores (A/B).
+static int out_tmap(CUtensorMap* tC, const HyGemmEpilogue* e, int M, int out_cols, GemmArgs& a) {
+  a.tma_out = 0;
+  if (e->out_f32 || e->row_map || ((uintptr_t)e->out & 15) || getenv("HY_GEMM_NOTMASTORE"))
+    return 0;
+  const int oc = e->act == HY_ACT_SWIGLU ? 16 : 32;
+  HY_RET_IF(make_tmap_2d_bf16(tC, e->out, M, out_cols, (uint64_t)e->ldc * 2, 32, oc, 0));
+  a.tma_out = 1;
+  return 0;
+}
 
 // Whole tiles before the stream-K part: all but the last 1-2 waves' worth, so every
 // stream-K share is >= one tile of k-blocks.  (Splitting only the remainder wave -- fewer
@@ -1013,12 +1104,15 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     // isolated was a trigger issued before the TMEM allocation, see gemm_tc_kernel)
     a.dbg = 0;
     if (const char* d = getenv("HY_PAIR_DBG")) a.dbg = atoi(d);
+    if (getenv("HY_GEMM_NOPREF")) a.dbg |= 4;  // A/B: no residual L2 prefetch
     if (const char* g = getenv("HY_GEMM_GROUP")) a.group = atoi(g);
     CUtensorMap tA, tB;
     HY_RET_IF(make_tmap_2d_bf16(&tA, A, M, K, (uint64_t)lda * 2, 128, 64));
     HY_RET_IF(make_tmap_2d_bf16(&tB, W, N, K, (uint64_t)ldw * 2, pair_bn / 2, 64));
-    const int rc = pair_bn == 128 ? launch_pair_epi<128>(epi, tA, tB, a, grid, st)
-                                  : launch_pair_epi<256>(epi, tA, tB, a, grid, st);
+    CUtensorMap tC = tA;
+    HY_RET_IF(out_tmap(&tC, e, M, out_cols, a));
+    const int rc = pair_bn == 128 ? launch_pair_epi<128>(epi, tA, tB, tC, a, grid, st)
+                                  : launch_pair_epi<256>(epi, tA, tB, tC, a, grid, st);
     if (rc < 0) {
       set_last_error("gemm: no pair kernel for this epilogue");
       return (int)cudaErrorInvalidValue;
@@ -1038,6 +1132,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     a.Q = N;
   }
   if (const char* env_bn = getenv("HY_GEMM_BN")) bn = atoi(env_bn);  // tuning only
+  if (getenv("HY_GEMM_NOPREF")) a.dbg |= 4;  // A/B: no residual L2 prefetch
   if (const char* g = getenv("HY_GEMM_GROUP")) a.group = atoi(g);
   a.np = ceil_div(a.P, 128);
   a.nq = ceil_div(a.Q, bn);
@@ -1080,8 +1175,10 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     HY_RET_IF(make_tmap_2d_bf16(&tA, W, N, K, (uint64_t)ldw * 2, 128, 64));
     HY_RET_IF(make_tmap_2d_bf16(&tB, A, M, K, (uint64_t)lda * 2, bn, 64));
   }
-  const int rc = swap ? launch_epi<true>(epi, bn, tA, tB, a, grid, st)
-                      : launch_epi<false>(epi, bn, tA, tB, a, grid, st);
+  CUtensorMap tC = tA;  // unused unless a.tma_out
+  if (!swap) HY_RET_IF(out_tmap(&tC, e, M, out_cols, a));
+  const int rc = swap ? launch_epi<true>(epi, bn, tA, tB, tC, a, grid, st)
+                      : launch_epi<false>(epi, bn, tA, tB, tC, a, grid, st);
   if (rc < 0) {
     set_last_error("gemm: no kernel for BN=" + std::to_string(bn));
     return (int)cudaErrorInvalidValue;

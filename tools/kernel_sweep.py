@@ -63,6 +63,7 @@ def timeit(fn, reps=5, per_graph=20, warm=3):
 
 
 VARIANTS = []
+RESIDUAL = []
 ONLY = []
 EXTRA = []
 
@@ -88,7 +89,13 @@ def gemm_sweep(out):
         Ws = [torch.randn(N, K, device=DEV).mul_(0.02).bfloat16() for _ in range(nw)]
         A = torch.randn(M, K, device=DEV).bfloat16()
         C = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
-        e = _lib.HyGemmEpilogue(0, 0, 0, 0, 0, C.data_ptr(), N, 0)
+        # in-place residual (the serving o / down projections: x += GEMM) when --residual
+        # names this shape; x rotates through buffers larger than L2 like the weights
+        if name in RESIDUAL or "all" in RESIDUAL:
+            R = torch.randn(M, N, device=DEV).bfloat16()
+            e = _lib.HyGemmEpilogue(0, R.data_ptr(), N, 0, 0, R.data_ptr(), N, 0)
+        else:
+            e = _lib.HyGemmEpilogue(0, 0, 0, 0, 0, C.data_ptr(), N, 0)
 
         def ours(i):
             W = Ws[i % nw]
@@ -311,11 +318,14 @@ def main():
     ap.add_argument("--variants", default="",
                     help="';'-separated env settings, e.g. 'HY_GEMM_NOSK=1;HY_GEMM_BN=128'")
     ap.add_argument("--only", default="", help="comma list of shape names")
+    ap.add_argument("--residual", default="", help="shape names run with an in-place residual "
+                    "epilogue ('all' for every shape)")
     ap.add_argument("--shapes", default="", help="extra MxNxK list, e.g. 128x128x64,577x1024x1024")
     args = ap.parse_args()
     for v in filter(None, args.variants.split(";")):
         VARIANTS.append(dict(kv.split("=") for kv in v.split(",")))
     ONLY.extend(filter(None, args.only.split(",")))
+    RESIDUAL.extend(filter(None, args.residual.split(",")))
     for x in filter(None, args.shapes.split(",")):
         M, N, K = (int(v) for v in x.split("x"))
         EXTRA.append(("custom", M, N, K))
