@@ -451,6 +451,7 @@ bool pdl_enabled();
 // fork a per-thread side stream off st (it waits for st's work so far) / join it back
 int side_fork(cudaStream_t st, cudaStream_t* side, cudaEvent_t* join);
 int side_join(cudaStream_t st, cudaStream_t side, cudaEvent_t join);
+int side_mark_and_wait(cudaStream_t from, cudaStream_t waiter);
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,

@@ -969,11 +969,15 @@ static int launch_epi(int epi, int bn, const CUtensorMap& tA, const CUtensorMap&
 static constexpr size_t kCounterBytes = 16384;
 
 // SMs a GEMM grid may occupy (HY_GEMM_SMS caps it, e.g. to leave SMs to a concurrent stream)
+static thread_local int t_sms_cap = 0;  // per-thread cap (split-mode forwards)
+void gemm_set_sms_cap(int sms) { t_sms_cap = sms; }
+
 static int gemm_sms() {
-  static const int cap = [] {
+  static const int env_cap = [] {
     const char* e = getenv("HY_GEMM_SMS");
     return e ? atoi(e) : 0;
   }();
+  const int cap = t_sms_cap > 0 ? (env_cap > 0 ? std::min(env_cap, t_sms_cap) : t_sms_cap) : env_cap;
   const int n = num_sms();
   return cap > 0 && cap < n ? cap : n;
 }

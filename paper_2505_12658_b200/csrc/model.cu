@@ -15,6 +15,7 @@
 namespace hy {
 int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K,
               const HyGemmEpilogue* e, void* ws, size_t ws_bytes, cudaStream_t st, int force_mode);
+void gemm_set_sms_cap(int sms);
 int rmsnorm(const void* x, int ldx, const void* w, void* out, int ldo, int rows, int cols,
             float eps, const int* row_idx, cudaStream_t st);
 int layernorm(const void* x, int ldx, const void* w, const void* b, void* out, int ldo, int rows,
@@ -27,12 +28,16 @@ int vit_gather_visual(const HyImageDesc* images, int n_images, int n_visual, int
 
 static constexpr size_t kGemmWs = 64ull << 20;  // split-K partials
 
-// Opt-in (HY_ATTN_FORK=1): measured on B200 (tools/mixed_batch.py, 64-256 decodes at ctx
-// 300-700 + 512-2816-token prefill chunks) the overlap is within +-2% of the serial order --
-// decode attention already fills every SM, so the prefill CTAs only fill its tail.
-static bool attn_fork_enabled() {
-  const char* e = getenv("HY_ATTN_FORK");
-  return e && e[0] == '1';
+// Split mode (two row groups on two streams, see hy_lang_forward): HY_LANG_SPLIT=<n> turns
+// it on for batches with >= n decode rows (0 / unset: off); HY_SPLIT_SMS SMs (default 24)
+// are kept free of GEMM CTAs for the other group's attention.
+static int split_min_decodes() {
+  const char* e = getenv("HY_LANG_SPLIT");
+  return e ? atoi(e) : 0;
+}
+static int split_reserve_sms() {
+  const char* e = getenv("HY_SPLIT_SMS");
+  return e ? atoi(e) : 24;
 }
 
 struct Carve {
@@ -52,7 +57,9 @@ struct LangWs {
   bf16 *x, *t, *qkv, *attn, *f, *tout;
   float* logits;
   void* gemm_ws;
+  void* gemm_ws2;
   void* dec_ws;
+  void* dec_ws2;
   size_t dec_ws_bytes;
 };
 
@@ -64,6 +71,7 @@ static size_t lang_carve(const HyLangModel* m, int max_rows, int max_out, int ma
   // the GEMM workspace holds stream-K arrival counters that must stay zero between
   // calls: it lives at a fixed offset (the start), independent of the batch shape
   l.gemm_ws = c.take<uint8_t>(kGemmWs);
+  l.gemm_ws2 = c.take<uint8_t>(kGemmWs);  // second row group's GEMMs (split mode)
   l.x = c.take<bf16>((size_t)max_rows * m->hidden);
   l.t = c.take<bf16>((size_t)max_rows * m->hidden);
   l.qkv = c.take<bf16>((size_t)max_rows * qkv_cols);
@@ -74,6 +82,7 @@ static size_t lang_carve(const HyLangModel* m, int max_rows, int max_out, int ma
   l.dec_ws_bytes =
       hy_attn_decode_workspace_bytes(std::max(max_decode, 1), m->n_heads, m->head_dim, max_ctx);
   l.dec_ws = c.take<uint8_t>(l.dec_ws_bytes);
+  l.dec_ws2 = c.take<uint8_t>(l.dec_ws_bytes);
   if (w) *w = l;
   return c.off + 256;
 }
@@ -105,7 +114,8 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
     return (int)cudaErrorInvalidValue;
   }
   auto G = [&](const bf16* A, int lda, const void* W, int M, int N, int K, const void* bias,
-               const void* res, int ldr, int act, void* out, int ldc, int f32) {
+               const void* res, int ldr, int act, void* out, int ldc, int f32, cudaStream_t s,
+               void* gws) {
     HyGemmEpilogue e{};
     e.bias = bias;
     e.residual = res;
@@ -114,10 +124,9 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
     e.out = out;
     e.ldc = ldc;
     e.out_f32 = f32;
-    timer_mark(HY_KCLASS_GEMM, st, true, 0.0);
-    int rc = gemm_bf16(A, lda, reinterpret_cast<const bf16*>(W), K, M, N, K, &e, w.gemm_ws,
-                       kGemmWs, st, 0);
-    timer_mark(HY_KCLASS_GEMM, st, false, 2.0 * M * N * K,
+    timer_mark(HY_KCLASS_GEMM, s, true, 0.0);
+    int rc = gemm_bf16(A, lda, reinterpret_cast<const bf16*>(W), K, M, N, K, &e, gws, kGemmWs, s, 0);
+    timer_mark(HY_KCLASS_GEMM, s, false, 2.0 * M * N * K,
                ((long long)M << 42) | ((long long)N << 21) | (long long)K);
     return rc;
   };
@@ -125,51 +134,89 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
   HY_RET_IF(hy_merge_embed(b->tok, R, m->embed, image_rows, H, last_tok, b->row_slot, w.x, st));
   const int nd = b->n_decode;
   const int np_rows = R - nd;
-  for (int li = 0; li < m->n_layers; ++li) {
+
+  // One layer over the rows [r0, r1): the first n_dec of them decode rows, the prefill rows
+  // (all of [nd, R)) included when r1 == R.  Every kernel addresses its rows by offset, so
+  // two disjoint row ranges can run on two streams at once.
+  // part 0: norm, QKV projection, RoPE + KV append; part 1: attention, O projection, MLP
+  auto layer = [&](int li, int part, int r0, int r1, int n_dec, cudaStream_t s, void* gws,
+                   void* dws) -> int {
     const HyLangLayerW& L = m->layers[li];
     bf16* kv_layer = reinterpret_cast<bf16*>(kv->base) + (size_t)li * kv->layer_stride;
-    HY_RET_IF(rmsnorm(w.x, H, L.attn_norm, w.t, H, R, H, m->rms_eps, nullptr, st));
-    HY_RET_IF(G(w.t, H, L.w_qkv, R, qkv_cols, H, L.b_qkv, nullptr, 0, HY_ACT_NONE, w.qkv,
-                qkv_cols, 0));
-    HY_RET_IF(hy_rope_kv_append(w.qkv, qkv_cols, R, m->n_heads, m->n_kv_heads, D, b->pos,
-                                b->row_slot, kv->block_table, kv->bt_stride, kv_layer,
-                                kv->block_stride, m->rope_theta, st));
-    // decode attention (HBM-bound) and prefill attention (tensor-bound) read disjoint rows
-    // of qkv and write disjoint rows of attn: the prefill part runs on a side stream so the
-    // two can overlap
-    const bool fork = nd > 0 && b->n_prefill > 0 && np_rows > 0 && attn_fork_enabled();
-    cudaStream_t pst = st;
-    cudaEvent_t join = nullptr;
-    if (fork) HY_RET_IF(side_fork(st, &pst, &join));
-    if (nd > 0) {
-      timer_mark(HY_KCLASS_DECODE_ATTN, st, true, 0.0);
-      HY_RET_IF(hy_attn_decode_paged(w.qkv, qkv_cols, nd, m->n_heads, m->n_kv_heads, D,
-                                     b->row_slot, b->dec_ctx, b->max_ctx, kv->block_table,
-                                     kv->bt_stride, kv_layer, kv->block_stride, scale, w.attn, QD,
-                                     w.dec_ws, w.dec_ws_bytes, st));
-      timer_mark(HY_KCLASS_DECODE_ATTN, st, false, 0.0);
+    const int rows = r1 - r0;
+    bf16* x = w.x + (size_t)r0 * H;
+    bf16* t = w.t + (size_t)r0 * H;
+    bf16* qkv = w.qkv + (size_t)r0 * qkv_cols;
+    bf16* attn = w.attn + (size_t)r0 * QD;
+    bf16* f = w.f + (size_t)r0 * m->ffn;
+    if (part == 0) {
+      HY_RET_IF(rmsnorm(x, H, L.attn_norm, t, H, rows, H, m->rms_eps, nullptr, s));
+      HY_RET_IF(G(t, H, L.w_qkv, rows, qkv_cols, H, L.b_qkv, nullptr, 0, HY_ACT_NONE, qkv,
+                  qkv_cols, 0, s, gws));
+      HY_RET_IF(hy_rope_kv_append(qkv, qkv_cols, rows, m->n_heads, m->n_kv_heads, D,
+                                  b->pos + r0, b->row_slot + r0, kv->block_table, kv->bt_stride,
+                                  kv_layer, kv->block_stride, m->rope_theta, s));
+      return 0;
     }
-    if (b->n_prefill > 0 && np_rows > 0) {
-      timer_mark(HY_KCLASS_PREFILL_ATTN, pst, true, 0.0);
-      HY_RET_IF(hy_attn_prefill_paged(w.qkv + (size_t)nd * qkv_cols, qkv_cols, np_rows, b->n_prefill,
-                                      b->pf_qstart, b->pf_offset, b->pf_slot, b->pf_max_q,
-                                      m->n_heads, m->n_kv_heads, D, kv->block_table,
+    if (n_dec > 0) {
+      timer_mark(HY_KCLASS_DECODE_ATTN, s, true, 0.0);
+      HY_RET_IF(hy_attn_decode_paged(qkv, qkv_cols, n_dec, m->n_heads, m->n_kv_heads, D,
+                                     b->row_slot + r0, b->dec_ctx + r0, b->max_ctx,
+                                     kv->block_table, kv->bt_stride, kv_layer, kv->block_stride,
+                                     scale, attn, QD, dws, w.dec_ws_bytes, s));
+      timer_mark(HY_KCLASS_DECODE_ATTN, s, false, 0.0);
+    }
+    if (r1 == R && b->n_prefill > 0 && np_rows > 0) {
+      timer_mark(HY_KCLASS_PREFILL_ATTN, s, true, 0.0);
+      HY_RET_IF(hy_attn_prefill_paged(w.qkv + (size_t)nd * qkv_cols, qkv_cols, np_rows,
+                                      b->n_prefill, b->pf_qstart, b->pf_offset, b->pf_slot,
+                                      b->pf_max_q, m->n_heads, m->n_kv_heads, D, kv->block_table,
                                       kv->bt_stride, kv_layer, kv->block_stride, scale,
-                                      w.attn + (size_t)nd * QD, QD, pst));
-      timer_mark(HY_KCLASS_PREFILL_ATTN, pst, false, 0.0);
+                                      w.attn + (size_t)nd * QD, QD, s));
+      timer_mark(HY_KCLASS_PREFILL_ATTN, s, false, 0.0);
     }
-    if (fork) HY_RET_IF(side_join(st, pst, join));
-    HY_RET_IF(G(w.attn, QD, L.w_o, R, H, QD, nullptr, w.x, H, HY_ACT_NONE, w.x, H, 0));
-    HY_RET_IF(rmsnorm(w.x, H, L.ffn_norm, w.t, H, R, H, m->rms_eps, nullptr, st));
-    HY_RET_IF(G(w.t, H, L.w_gate_up, R, 2 * m->ffn, H, nullptr, nullptr, 0, HY_ACT_SWIGLU, w.f,
-                m->ffn, 0));
-    HY_RET_IF(G(w.f, m->ffn, L.w_down, R, H, m->ffn, nullptr, w.x, H, HY_ACT_NONE, w.x, H, 0));
+    HY_RET_IF(G(attn, QD, L.w_o, rows, H, QD, nullptr, x, H, HY_ACT_NONE, x, H, 0, s, gws));
+    HY_RET_IF(rmsnorm(x, H, L.ffn_norm, t, H, rows, H, m->rms_eps, nullptr, s));
+    HY_RET_IF(G(t, H, L.w_gate_up, rows, 2 * m->ffn, H, nullptr, nullptr, 0, HY_ACT_SWIGLU, f,
+                m->ffn, 0, s, gws));
+    HY_RET_IF(G(f, m->ffn, L.w_down, rows, H, m->ffn, nullptr, x, H, HY_ACT_NONE, x, H, 0, s, gws));
+    return 0;
+  };
+
+  const int split_min = split_min_decodes();
+  if (split_min > 0 && nd >= split_min) {
+    // Two row groups on two streams (first half of the decode rows | the rest + prefill):
+    // while one group's decode attention streams KV from HBM, the other group's GEMMs keep
+    // the tensor cores busy.  GEMM grids leave split_reserve_sms() SMs to the attention.
+    const int na = nd / 2;
+    cudaStream_t side = nullptr;
+    cudaEvent_t join = nullptr;
+    HY_RET_IF(side_fork(st, &side, &join));
+    gemm_set_sms_cap(num_sms() - split_reserve_sms());
+    // group A (side stream) starts half a layer ahead: group B's first QKV projection waits
+    // for A's, so from then on A's attention meets B's GEMMs and vice versa
+    int rc = layer(0, 0, 0, na, na, side, w.gemm_ws2, w.dec_ws2);
+    if (rc == 0) rc = side_mark_and_wait(side, st);
+    for (int li = 0; li < m->n_layers && rc == 0; ++li) {
+      rc = layer(li, 1, 0, na, na, side, w.gemm_ws2, w.dec_ws2);
+      if (rc == 0 && li + 1 < m->n_layers) rc = layer(li + 1, 0, 0, na, na, side, w.gemm_ws2, w.dec_ws2);
+      if (rc == 0) rc = layer(li, 0, na, R, nd - na, st, w.gemm_ws, w.dec_ws);
+      if (rc == 0) rc = layer(li, 1, na, R, nd - na, st, w.gemm_ws, w.dec_ws);
+    }
+    gemm_set_sms_cap(0);
+    HY_RET_IF(rc);
+    HY_RET_IF(side_join(st, side, join));
+  } else {
+    for (int li = 0; li < m->n_layers; ++li) {
+      HY_RET_IF(layer(li, 0, 0, R, nd, st, w.gemm_ws, w.dec_ws));
+      HY_RET_IF(layer(li, 1, 0, R, nd, st, w.gemm_ws, w.dec_ws));
+    }
   }
   if (b->n_out > 0) {
     HY_RET_IF(rmsnorm(w.x, H, m->final_norm, w.tout, H, b->n_out, H, m->rms_eps, b->out_rows, st));
     float* logits = b->out_logits ? b->out_logits : w.logits;
     HY_RET_IF(G(w.tout, H, m->lm_head, b->n_out, m->vocab, H, nullptr, nullptr, 0, HY_ACT_NONE,
-                logits, m->vocab, 1));
+                logits, m->vocab, 1, st, w.gemm_ws));
     HY_RET_IF(hy_argmax_f32(logits, b->n_out, m->vocab, m->vocab, b->out_tokens, b->out_slot,
                             last_tok, st));
   }

@@ -159,6 +159,15 @@ int side_fork(cudaStream_t st, cudaStream_t* side, cudaEvent_t* join) {
   return 0;
 }
 
+// `waiter` waits for the work enqueued on `from` so far (one extra event per thread)
+int side_mark_and_wait(cudaStream_t from, cudaStream_t waiter) {
+  thread_local cudaEvent_t ev = nullptr;
+  if (!ev) HY_CUDA_RET(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  HY_CUDA_RET(cudaEventRecord(ev, from));
+  HY_CUDA_RET(cudaStreamWaitEvent(waiter, ev, 0));
+  return 0;
+}
+
 int side_join(cudaStream_t st, cudaStream_t side, cudaEvent_t join) {
   HY_CUDA_RET(cudaEventRecord(join, side));
   HY_CUDA_RET(cudaStreamWaitEvent(st, join, 0));

@@ -143,3 +143,16 @@ def test_measured_clock_runs_and_reports():
         assert rep.aggregates["n_finished"] == len(g["requests"])
         assert cl.transfer_stats["count"] > 0
         assert rep.aggregates["token_throughput_tps"] > 0
+
+
+def test_split_row_groups_parity(monkeypatch):
+    """HY_LANG_SPLIT: the decoder runs two row groups on two streams (opt-in; measured slower
+    on B200, tools/mixed_batch.py) -- same scheduler decisions and logits as the one-stream
+    path."""
+    monkeypatch.setenv("HY_LANG_SPLIT", "2")
+    shape = get_shape("tiny")
+    g, cl, _ = _run("config1_2000rps", shape)
+    assert batch_log_digest(cl.batch_log) == g["sha"]
+    res = oracle_replay(cl, shape, seed=0)
+    assert res["max_abs_err"] <= LOGIT_ATOL, res
+    assert res["tokens_equal"] + res["near_ties"] == res["rows"], res

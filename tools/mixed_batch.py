@@ -1,6 +1,6 @@
 """Device time of mixed decode + prefill batches on the LLaVA-1.5-7B EPD instance, for A/B
-comparisons of environment knobs read per call (e.g. HY_ATTN_FORK=1).
-    python tools/mixed_batch.py [--reps 7] [--variants 'HY_ATTN_FORK=1;...']"""
+comparisons of environment knobs read per call (e.g. HY_LANG_SPLIT=16).
+    python tools/mixed_batch.py [--reps 7] [--variants 'HY_LANG_SPLIT=16;...']"""
 import argparse
 import os
 import sys
@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=7)
-    ap.add_argument("--variants", default="HY_ATTN_FORK=1")
+    ap.add_argument("--variants", default="HY_LANG_SPLIT=16")
     args = ap.parse_args()
     import paper_2505_12658_b200 as P
     from paper_2505_12658_b200._epdsim import C, E, EN, MC
