@@ -98,6 +98,7 @@ class GpuCluster(C.Cluster):
         self.batch_log: Optional[List] = [] if record_batches else None
         self.migration_log: List = []
         self.transfer_stats = {"count": 0, "bytes": 0.0, "copied_bytes": 0, "seconds": 0.0}
+        self._live = None  # {iid: in-flight batch} while live.run_live drives the cluster
         self.generated: Dict[str, List[int]] = {}
         # per-batch budgets: the reference's roofline search (decisions identical to the
         # reference) or the same search over GPU-timed probe batches
@@ -115,6 +116,15 @@ class GpuCluster(C.Cluster):
         self._admit_migrations(inst)
         batch = inst.form_batch(self.reqs)
         if not batch:
+            return
+        if self._live is not None:  # live.run_live: launch, complete on the CUDA events
+            self._live[iid] = self.runtimes[iid].launch_batch(batch, self.reqs, self.clock,
+                                                             self.model, self.hw)
+            if self.capture:
+                self.exec_order.append((iid, len(self.runtimes[iid].exec_log)))
+            inst.busy = True
+            inst.current_batch = batch
+            inst.current_latency = 0.0
             return
         latency = self.runtimes[iid].run_batch(batch, self.reqs, self.clock, self.model,
                                                self.hw)
@@ -204,6 +214,10 @@ class GpuCluster(C.Cluster):
 
     def run(self, trace, check_invariants: bool = False):
         report = super().run(trace, check_invariants=check_invariants)
+        self._collect_generated()
+        return report
+
+    def _collect_generated(self) -> None:
         merged: Dict[str, List] = {}
         for rt in self.runtimes.values():
             rt.collect_tokens(rt.generated)
@@ -212,7 +226,6 @@ class GpuCluster(C.Cluster):
             rt.generated.clear()
         for rid, toks in merged.items():
             self.generated[rid] = [t for _, t in sorted(toks)]
-        return report
 
     def _assert_invariants(self) -> None:
         super()._assert_invariants()

@@ -26,6 +26,7 @@ It never mutates ``batch`` or ``reqs`` (the loop does that in ``_on_batch_done``
 
 from __future__ import annotations
 
+import dataclasses
 import itertools
 import os
 import time
@@ -45,6 +46,24 @@ IMG = MC.IMAGE_BLOCK_TOKENS
 KVB = MC.KV_BLOCK_TOKENS
 CLOCKS = ("oracle", "device", "wall")
 _BATCH_SEQ = itertools.count()  # global batch order, to merge tokens across instances
+
+
+@dataclasses.dataclass
+class _Inflight:
+    """A launched batch: what ``complete_batch`` needs to account it."""
+    batch: object
+    reqs: dict
+    clock: str
+    model_profile: object
+    hw: object
+    t_host0: float
+    has_lang: bool
+    has_vis: bool
+    n_out: int
+    tok_off: int
+    out_rids: list
+    cap_logits: object
+    host_tokens: object = None  # pinned D2H buffer of the step's tokens (clock="wall")
 
 
 class _Staging:
@@ -321,7 +340,18 @@ class InstanceRuntime:
 
     # ------------------------------------------------------------------ execute
     def run_batch(self, batch, reqs, clock: str, model_profile=None, hw=None) -> float:
+        """Launch one batch, wait for it and return its latency under ``clock``."""
+        return self.complete_batch(self.launch_batch(batch, reqs, clock, model_profile, hw))
+
+    def batch_done(self) -> bool:
+        """True once the batch in flight (``launch_batch``) has finished on both streams."""
+        return self.ev_l.query() and self.ev_v.query()
+
+    def launch_batch(self, batch, reqs, clock: str, model_profile=None, hw=None) -> "_Inflight":
+        """Lower and launch one batch on the V/L streams without waiting for it (at most one
+        batch in flight per instance: the reference marks the instance busy)."""
         t_host0 = time.perf_counter()
+        cap_logits = None
         lib = self.lib
         dev = self.device
         sl, sv = self.stream_l, self.stream_v
@@ -373,11 +403,20 @@ class InstanceRuntime:
         if n_out:
             self.tok_records.append((tok_off, out_rids, next(_BATCH_SEQ)))
             self.tok_cursor += n_out
+        host = None
         if clock == "wall" and n_out:
             # end-to-end: read this step's tokens back to the host
             host = torch.empty(n_out, dtype=torch.int32, pin_memory=True)
             with torch.cuda.stream(sl):
                 host.copy_(self.tok_log[tok_off:tok_off + n_out], non_blocking=True)
+        return _Inflight(batch, reqs, clock, model_profile, hw, t_host0, has_lang, has_vis,
+                         n_out, tok_off, out_rids, cap_logits, host)
+
+    def complete_batch(self, h: "_Inflight") -> float:
+        """Wait for the batch ``h`` and account it; returns its latency under ``h.clock``."""
+        batch, reqs, clock, has_lang, has_vis = h.batch, h.reqs, h.clock, h.has_lang, h.has_vis
+        n_out, tok_off, out_rids, cap_logits = h.n_out, h.tok_off, h.out_rids, h.cap_logits
+        t_host0, sampler = h.t_host0, self.sampler
         self.ev_v.synchronize()
         self.ev_l.synchronize()
         t_l = self.ev_start.elapsed_time(self.ev_l)
@@ -416,7 +455,7 @@ class InstanceRuntime:
             return dev_ms * 1e-3
         if clock == "wall":
             return host_s
-        return EN.batch_latency(batch, reqs, model_profile, hw)
+        return EN.batch_latency(batch, reqs, h.model_profile, h.hw)
 
     def _run_vision(self, batch, reqs, sv) -> None:
         s = self.shape
