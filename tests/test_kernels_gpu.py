@@ -226,7 +226,8 @@ def test_prefill_attention_paged(n_heads, n_kv, chunks, tiles, monkeypatch):
     kv, bt, bts, be = _paged_setup(n, ctxs, n_kv, d, L, layer, seed=1)
     rows = sum(c for _, c in chunks)
     # scaled queries: the running row max jumps across KV tiles (online-softmax rescale path)
-    q = (torch.randn(rows, n_heads * d, device=DEV) * 3).bfloat16()
+    g = torch.Generator(device=DEV).manual_seed(rows * 31 + n_heads)
+    q = (torch.randn(rows, n_heads * d, device=DEV, generator=g) * 3).bfloat16()
     out = torch.empty(rows, n_heads * d, device=DEV, dtype=torch.bfloat16)
     qstart = torch.tensor(np.cumsum([0] + [c for _, c in chunks]), dtype=torch.int32, device=DEV)
     offs = torch.tensor([o for o, _ in chunks], dtype=torch.int32, device=DEV)
@@ -244,7 +245,12 @@ def test_prefill_attention_paged(n_heads, n_kv, chunks, tiles, monkeypatch):
         mask = torch.arange(o + c, device=DEV)[None] > (o + torch.arange(c, device=DEV))[:, None]
         s = s.masked_fill(mask[None], float("-inf"))
         ref = torch.einsum("hqt,thd->qhd", torch.softmax(s, -1), V.repeat_interleave(grp, 1))
-        assert (out[r0:r0 + c].float() - ref.reshape(c, -1)).abs().max().item() < 2e-2, i
+        # bf16 P and bf16 output: 2e-2 absolute plus 1e-2 relative (with x3 queries the
+        # outputs reach |3|, where one bf16 ulp is 0.016; 0.023 seen on one element in 40
+        # seeds of the 616-token case, identical for 1 and 2 query tiles per CTA)
+        ref = ref.reshape(c, -1)
+        err = (out[r0:r0 + c].float() - ref).abs() - 1e-2 * ref.abs()
+        assert err.max().item() < 2e-2, i
         r0 += c
 
 
