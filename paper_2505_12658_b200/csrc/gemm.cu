@@ -336,6 +336,19 @@ __device__ __forceinline__ void add_partials(float* v, const float4* const* srcs
   }
 }
 
+// Stream-K: true when every other contributor of this tile has already published its
+// partial (arrival counter == others), checked only for a CTA's last segment (slot 1), the
+// one that normally completes last.  The acquire load orders the partial reads after the
+// others' fenced stores; the caller then finishes the tile without publishing its own.
+__device__ __forceinline__ bool sk_all_arrived(int* ctr, int others, int slot, int lane) {
+  if (slot != 1) return false;
+  int v = 0;
+  if (lane == 0) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+  const bool all = __shfl_sync(0xffffffffu, v, 0) == others;
+  if (all) __threadfence();  // every lane's partial loads after the others' stores
+  return all;
+}
+
 struct Seg {
   int tile;      // raster index
   int kb0, kb1;  // k-block range
@@ -555,35 +568,38 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
       int c0 = 0, c1 = -1;
       long long ub = 0;
       if (sg.slot >= 0) {
-        // stream-K partial: publish raw accumulators, then count arrivals
-        // layout [cta][slot][chunk][j/4][128 rows] float4: lane-consecutive 16B stores
-        float4* mine = reinterpret_cast<float4*>(a.partial) +
-                       (size_t)(cta * 2 + sg.slot) * (BN / 32) * 8 * 128 + lrow;
-#pragma unroll 1
-        for (int c = half; c < BN / 32; c += 2) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(taddr + c * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            __stcg(mine + (c * 8 + j / 4) * 128,
-                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                               __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
-        }
         ub = (long long)sg.sk * a.nkb;
         c0 = (int)(((ub + 1) * G - 1) / a.u_sk);
         c1 = (int)(((ub + a.nkb) * G - 1) / a.u_sk);
-        __threadfence();
-        __syncwarp();
-        int prev = 0;
         int* ctr = a.counters + sg.sk * 8 + half * 4 + sub;
-        if (lane == 0) prev = atomicAdd(ctr, 1);
-        prev = __shfl_sync(0xffffffffu, prev, 0);
-        finish = prev == c1 - c0;  // the last contributor reduces and writes the tile
-        if (finish) {
+        // the CTA's last segment usually finishes after every other contributor of its
+        // tile: then it skips publishing its own partial (the end-of-kernel burst of
+        // partial traffic, when every CTA finishes at once, is what made stream-K slow)
+        if (!sk_all_arrived(ctr, c1 - c0, sg.slot, lane)) {
+          // stream-K partial: publish raw accumulators, then count arrivals
+          // layout [cta][slot][chunk][j/4][128 rows] float4: lane-consecutive 16B stores
+          float4* mine = reinterpret_cast<float4*>(a.partial) +
+                         (size_t)(cta * 2 + sg.slot) * (BN / 32) * 8 * 128 + lrow;
+#pragma unroll 1
+          for (int c = half; c < BN / 32; c += 2) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(taddr + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              __stcg(mine + (c * 8 + j / 4) * 128,
+                     make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                 __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+          }
           __threadfence();
-          if (lane == 0) *ctr = 0;  // ready for the next GEMM on this workspace
+          __syncwarp();
+          int prev = 0;
+          if (lane == 0) prev = atomicAdd(ctr, 1);
+          prev = __shfl_sync(0xffffffffu, prev, 0);
+          finish = prev == c1 - c0;  // the last contributor reduces and writes the tile
+          if (finish) __threadfence();
         }
+        if (finish && lane == 0) *ctr = 0;  // ready for the next GEMM on this workspace
       }
       if (finish) {
 #pragma unroll 1
@@ -819,34 +835,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
       long long ub = 0;
       if (sg.slot >= 0) {
         // stream-K partial of this CTA's 128 rows: [pair][slot][rank][chunk][j/4][row] float4
-        float4* mine = reinterpret_cast<float4*>(a.partial) +
-                       ((size_t)(pair * 2 + sg.slot) * 2 + rank) * (BN / 32) * 8 * 128 + lrow;
-#pragma unroll 1
-        for (int c = half; c < BN / 32; c += 2) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(taddr + c * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            __stcg(mine + (c * 8 + j / 4) * 128,
-                   make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                               __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
-        }
         ub = (long long)sg.sk * a.nkb;
         c0 = (int)(((ub + 1) * npairs - 1) / a.u_sk);
         c1 = (int)(((ub + a.nkb) * npairs - 1) / a.u_sk);
-        __threadfence();
-        __syncwarp();
-        int prev = 0;
         int* ctr = a.counters + sg.sk * 16 + rank * 8 + half * 4 + sub;
-        if (lane == 0) prev = atomicAdd(ctr, 1);
-        prev = __shfl_sync(0xffffffffu, prev, 0);
-        finish = prev == c1 - c0;  // the last contributing pair reduces and writes the rows
-        if (finish && lane == 0 && sub == 0 && half == 0) HY_CINC(5);
-        if (finish) {
+        if (!sk_all_arrived(ctr, c1 - c0, sg.slot, lane)) {  // see gemm_tc_kernel
+          float4* mine = reinterpret_cast<float4*>(a.partial) +
+                         ((size_t)(pair * 2 + sg.slot) * 2 + rank) * (BN / 32) * 8 * 128 + lrow;
+#pragma unroll 1
+          for (int c = half; c < BN / 32; c += 2) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(taddr + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              __stcg(mine + (c * 8 + j / 4) * 128,
+                     make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                 __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+          }
           __threadfence();
-          if (lane == 0) *ctr = 0;
+          __syncwarp();
+          int prev = 0;
+          if (lane == 0) prev = atomicAdd(ctr, 1);
+          prev = __shfl_sync(0xffffffffu, prev, 0);
+          finish = prev == c1 - c0;  // the last contributing pair reduces and writes the rows
+          if (finish) __threadfence();
         }
+        if (finish && lane == 0 && sub == 0 && half == 0) HY_CINC(5);
+        if (finish && lane == 0) *ctr = 0;
       }
       if (finish) {
 #pragma unroll 1
