@@ -281,13 +281,18 @@ def overlap_probe(out):
 def decode_sweep(out):
     """Paged decode attention (K8) bandwidth for MHA (LLaVA) and GQA (Qwen2-VL 28/4)."""
     import math
-    for nh, nkv, n, ctx in ((32, 32, 256, 660), (28, 4, 256, 660), (28, 4, 64, 4000),
-                            (32, 8, 256, 660), (32, 32, 16, 8000)):
+    for nh, nkv, n, ctx, shuffled in ((32, 32, 256, 660, 0), (32, 32, 256, 660, 1),
+                                      (32, 32, 128, 700, 1), (32, 32, 64, 700, 1),
+                                      (32, 32, 32, 700, 1), (28, 4, 256, 660, 0),
+                                      (28, 4, 64, 4000, 0), (32, 8, 256, 660, 0),
+                                      (32, 32, 16, 8000, 0)):
         d = 128
         nb = -(-ctx // 16)
         be = 2 * nkv * 16 * d
         kv = torch.randn(n * nb + 1, be, device=DEV).bfloat16()
-        bt = torch.arange(n * nb, dtype=torch.int32, device=DEV).view(n, nb).contiguous()
+        # shuffled: blocks scattered over the pool as the free list hands them out in serving
+        ids = torch.randperm(n * nb, device=DEV) if shuffled else torch.arange(n * nb, device=DEV)
+        bt = ids.to(torch.int32).view(n, nb).contiguous()
         q = torch.randn(n, nh * d, device=DEV).bfloat16()
         o = torch.empty_like(q)
         slots = torch.arange(n, dtype=torch.int32, device=DEV)
@@ -304,9 +309,9 @@ def decode_sweep(out):
         t = timeit(ours)
         byt = n * ctx * 2 * nkv * d * 2
         r = {"name": "decode_attn", "n_heads": nh, "n_kv": nkv, "seqs": n, "ctx": ctx,
-             "us": t * 1e3, "gbs": byt / t / 1e6}
+             "shuffled_blocks": bool(shuffled), "us": t * 1e3, "gbs": byt / t / 1e6}
         out.append(r)
-        print(f"decode_attn heads {nh}/{nkv} seqs {n} ctx {ctx}: {t*1e3:8.1f} us "
+        print(f"decode_attn heads {nh}/{nkv} seqs {n} ctx {ctx}{' shuffled' if shuffled else ''}: {t*1e3:8.1f} us "
               f"{r['gbs']:7.0f} GB/s", flush=True)
         del kv
 
