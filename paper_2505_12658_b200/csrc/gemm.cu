@@ -997,8 +997,11 @@ static int gemm_sms() {
   const int n = num_sms();
   return cap > 0 && cap < n ? cap : n;
 }
-// token rows from which the CTA-pair kernel is used (tuned on B200, tools/kernel_sweep.py)
-static constexpr int kPairMinRows = 512;
+// token rows from which the CTA-pair kernel is considered (tuned on B200,
+// tools/kernel_sweep.py): from 385 rows the 256-row pair tiles cover the 128-row tiles
+// without a half-empty pair row (M = 450-511: qkv / gate_up / down 8-16% faster as pairs;
+// M = 257-384 stays single-CTA, where the pair lost up to 35%)
+static constexpr int kPairMinRows = 385;
 
 // Output map for the normal orientation's TMA-store epilogue: bf16 output without a row
 // map, 16B-aligned base (ldc % 8 == 0 is checked by the caller); box 32 rows x 32 outputs

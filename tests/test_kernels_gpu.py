@@ -84,6 +84,7 @@ def _gemm_ref(A, W, bias, act, res):
     (300, 1024, 1024, 3, 2, True, True, False),
     (260, 32000, 512, 3, 0, False, False, True),
     (4096, 12288, 4096, 0, 0, False, False, False),    # heuristic picks the pair kernel
+    (450, 4096, 1024, 0, 0, True, True, False),        # pair from 385 rows, ragged last pair row
     (2816, 4096, 4096, 0, 0, False, True, False),      # heuristic: pair kernel, 128-wide tiles
     (700, 1408, 1024, 3, 4, False, False, False),      # forced pair, N % 256 != 0 -> BN 128
     (3000, 4096, 4096, 3, 0, True, True, False),       # pair; + stream-K tail below
