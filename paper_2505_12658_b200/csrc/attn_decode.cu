@@ -492,9 +492,19 @@ __global__ void attn_decode_combine_kernel(const float* __restrict__ part, int n
   out[(size_t)b * ld_o + (size_t)h * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
 }
 
-static int decode_splits(int n, int n_kv, int max_ctx) {
+// KV splits per (sequence, KV head): enough CTAs for ~per_sm per SM.  GQA CTAs (G >= 4
+// query heads per KV head, tensor-core kernel) aim for 4 per SM -- each already does G
+// heads of work per byte, and fewer splits save the combine pass (Qwen2-VL 28/4, 256 x 660
+// context: 70 us at 4 vs 83 us at 8, 5.7 vs 5.4 TB/s at 64 x 4000); MHA keeps 8
+// (tools/kernel_sweep.py --what decode; HY_DECODE_CTAS_PER_SM overrides for A/B).
+static int decode_splits(int n, int n_kv, int max_ctx, int G = 1) {
   const int max_blocks = std::max(1, ceil_div(max_ctx, HY_KV_BLOCK_TOKENS));
-  const int target = num_sms() * 8;
+  static const int env_per_sm = [] {
+    const char* e = getenv("HY_DECODE_CTAS_PER_SM");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  const int per_sm = env_per_sm ? env_per_sm : (G >= 4 ? 4 : 8);
+  const int target = num_sms() * per_sm;
   int ns = ceil_div(target, std::max(1, n * n_kv));
   ns = std::min(ns, std::max(1, max_blocks / 4));  // >= 4 blocks per split: one per warp
   return std::max(1, std::min(ns, 64));
@@ -518,7 +528,7 @@ extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads,
   HY_CHECK_ARG(n_kv_heads > 0 && n_heads % n_kv_heads == 0, "heads");
   if (n <= 0) return 0;
   const int G = n_heads / n_kv_heads;
-  int ns = decode_splits(n, n_kv_heads, max_ctx);
+  int ns = decode_splits(n, n_kv_heads, max_ctx, G);
   const size_t need = (size_t)n * n_heads * ns * (head_dim + 2) * sizeof(float);
   if (ns > 1 && (workspace == nullptr || need > workspace_bytes)) ns = 1;
   const int max_blocks = std::max(1, ceil_div(max_ctx, HY_KV_BLOCK_TOKENS));
