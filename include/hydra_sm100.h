@@ -21,8 +21,12 @@
  *   - every entry point returns 0 or a cudaError_t code; hy_last_error() gives text;
  *   - every pointer is device memory (or a mapped peer pointer) unless stated;
  *   - int32 metadata arrays are device resident; host arrays are marked "host";
- *   - no global state beyond cached kernel attributes: any host thread may call with
- *     its own stream;
+ *   - any host thread may call with its own stream, on any device.  Process-wide state is
+ *     limited to: the per-(device, kernel) shared-memory attribute cache (mutex guarded),
+ *     one side stream + events per (host thread, device, priority), tuning knobs read once
+ *     from the environment (HY_*; defaults are the measured best), the launch counter
+ *     (hy_launch_count) and the optional kernel timer hook (hy_set_kernel_timer, a
+ *     bench/test instrument that must not be set while several threads launch);
  *   - nothing falls back to the CPU: a missing device or bad argument is an error.
  *
  * Paged layouts (one instance = one GPU)
@@ -181,6 +185,17 @@ int hy_im2col_patches(const HyImageDesc* images, int n_images, int n_patches, in
  * Pointers may be peer (NVLink) addresses.  ids are device int32 arrays. */
 int hy_copy_blocks(const void* src_base, void* dst_base, const int* src_ids, const int* dst_ids,
                    int n, long long block_bytes, cudaStream_t stream);
+
+/* Token-exact variant (SURVEY.md 8b `valid_tail_bytes`): blocks 0..n-2 are copied whole; the
+ * last block is viewed as block_bytes / group_bytes groups and only the first
+ * tail_group_bytes of each group are copied.  KV block [layers][K|V][kv_heads][16][d]:
+ * group = 16*d*2 bytes, tail = valid_tokens*d*2, so the bytes moved equal the reference's
+ * MigrationJob.kv_bytes (cluster.py:411, migration.py:63-64).  Image block [576][H]: group =
+ * block, tail = valid_rows*H*2.  Records whose size is not a multiple of 16 bytes (e.g. a
+ * 4-byte last-token slot) are copied whole with group = tail = block_bytes. */
+int hy_copy_blocks_tail(const void* src_base, void* dst_base, const int* src_ids,
+                        const int* dst_ids, int n, long long block_bytes, long long group_bytes,
+                        long long tail_group_bytes, cudaStream_t stream);
 
 /* peer access for P2P block copies between GPUs driven by one process */
 int hy_enable_peer_access(int device, int peer);

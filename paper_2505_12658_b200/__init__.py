@@ -13,9 +13,10 @@ Public API
   b200_hardware                  HardwareProfile for one B200
 """
 
-from . import _lib
-
-_lib.load()  # fail loudly at import when the CUDA library is missing (no CPU fallback)
+from . import _lib  # noqa: F401  (the .so loads on first device use: GpuCluster,
+#                     InstanceRuntime, DeviceWeights; a missing library raises there --
+#                     there is no CPU fallback -- while the host-only modules (shapes,
+#                     inputs, planner) stay importable without mapping it)
 
 from ._epdsim import E as epdsim  # noqa: E402
 from .shapes import MllmShape, PRESETS, get_shape, with_layers  # noqa: E402

@@ -135,6 +135,8 @@ _SIGS = {
                                   c_void_p]),
     "hy_copy_blocks": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_longlong,
                                c_void_p]),
+    "hy_copy_blocks_tail": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_longlong,
+                                    c_longlong, c_longlong, c_void_p]),
     "hy_enable_peer_access": (c_int, [c_int, c_int]),
     "hy_scatter_i32": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "hy_fill_uniform_bf16": (c_int, [c_void_p, c_longlong, c_longlong, c_longlong, c_ulonglong,

@@ -28,6 +28,7 @@ import hashlib
 import json
 from typing import Dict, List, Optional, Sequence
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -57,7 +58,7 @@ class GpuMigrationJob(MG.MigrationJob):
 class GpuCluster(C.Cluster):
     def __init__(self, spec, shape: MllmShape, hw, slo, *, devices: Sequence = None,
                  clock: str = "device", seed: int = 0, resident_inputs: bool = True,
-                 probe_image_tokens: int = MC.IMAGE_BLOCK_TOKENS, max_slots: int = 4096,
+                 probe_image_tokens: int = MC.IMAGE_BLOCK_TOKENS, max_slots: Optional[int] = None,
                  max_seq_tokens: int = 16384, record_batches: bool = False,
                  weights: Optional[Dict] = None, capture: bool = False,
                  pool_bytes_limit: Optional[int] = None, profile_override=None,
@@ -78,8 +79,9 @@ class GpuCluster(C.Cluster):
         self.images = ImageStore(seed, shape.patch)
         self.weights: Dict[torch.device, DeviceWeights] = dict(weights or {})
         self.runtimes: Dict[str, InstanceRuntime] = {}
-        for k, (iid, inst) in enumerate(self.instances.items()):
-            dev = devices[k % len(devices)]
+        place = instance_devices(list(self.instances), devices)
+        for iid, inst in self.instances.items():
+            dev = place[iid]
             if dev not in self.weights:
                 self.weights[dev] = DeviceWeights(shape, dev, seed)
             self.runtimes[iid] = InstanceRuntime(
@@ -147,64 +149,95 @@ class GpuCluster(C.Cluster):
         self.jobs[r.rid] = GpuMigrationJob(**fields).bind(self)
 
     def _execute_transfer(self, job: GpuMigrationJob, hw) -> float:
+        """Launch the job's block copy on the target's copy stream (pull: the target GPU's
+        SMs read the source pool, through a peer NVLink pointer when the instances sit on
+        different GPUs) and return its duration under the cluster clock.
+
+        Token-exact: whole blocks except the last one, of which only the valid tokens (KV)
+        or rows (image) move, so the bytes copied equal ``job.kv_bytes + job.image_bytes``
+        (cluster.py:411-413).  Ordering is by events, never a device-wide sync: the copy
+        waits for the source's last batch; both instances' next batches wait for the copy
+        (the target reads the blocks, the source may reuse them once it releases them at
+        MIG_DONE).  clock="device" waits for the copy's completion event to charge the
+        measured time; in live mode (live.py) nothing waits here -- MIG_DONE is delivered
+        when the completion event fires."""
         src = self.runtimes[job.source]
         dst = self.runtimes[job.target]
         r = self.reqs[job.rid]
         lib = _lib.load()
-        kv_n = MC.kv_blocks_needed(r.kv_len) if job.kv_bytes > 0 else 0
-        img_n = job.image_blocks if job.image_bytes > 0 else 0
-        maps = []
-        if kv_n:
-            s_ids = src.kv_pool.ids[job.rid][:kv_n]
-            d_ids = dst.kv_pool.ids[job.rid][:kv_n]
-            maps.append(("kv", s_ids, d_ids, src.kv, dst.kv, self.shape.kv_block_elems * 2))
-        if img_n:
-            s_ids = src.image_pool.ids[job.rid][:img_n]
-            d_ids = dst.image_pool.ids[job.rid][:img_n]
-            maps.append(("image", s_ids, d_ids, src.img, dst.img,
-                         self.shape.image_block_elems * 2))
-        dev = dst.device  # pull-based: the target's SMs read the source pool
-        torch.cuda.set_device(dev)
-        stream = torch.cuda.current_stream(dev)
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ids_dev = []
-        for _, s_ids, d_ids, *_ in maps:
-            ids_dev.append(torch.tensor(list(s_ids) + list(d_ids), dtype=torch.int32).to(dev))
-        # the source's last batch must be complete before its blocks are read
-        torch.cuda.synchronize(src.device)
-        ev0.record(stream)
-        copied = 0
-        for (what, s_ids, d_ids, s_pool, d_pool, block_bytes), ids in zip(maps, ids_dev):
-            n = len(s_ids)
-            _lib.check(lib.hy_copy_blocks(s_pool.data_ptr(), d_pool.data_ptr(), ids.data_ptr(),
-                                          ids.data_ptr() + 4 * n, n, block_bytes,
-                                          stream.cuda_stream), "hy_copy_blocks")
-            copied += n * block_bytes
-        if job.kind == "pd":
-            ss = src.kv_pool.slot[job.rid]
-            ds = dst.kv_pool.slot[job.rid]
-            dst.last_tok[ds:ds + 1].copy_(src.last_tok[ss:ss + 1], non_blocking=True)
-        ev1.record(stream)
-        ev1.synchronize()
-        ms = ev0.elapsed_time(ev1)
+        bases = {"kv": (src.kv, dst.kv), "image": (src.img, dst.img),
+                 "last_tok": (src.last_tok, dst.last_tok)}
+        maps = [(w, a, b_) + bases[w] + (blk, grp, tail) for w, a, b_, blk, grp, tail in
+                plan_transfer(job, r, self.shape, src.kv_pool, dst.kv_pool, src.image_pool,
+                              dst.image_pool)]
+        dev = dst.device
+        st = dst.copy_stream()
+        ids_host = np.concatenate([np.asarray(list(m[1]) + list(m[2]), dtype=np.int32)
+                                   for m in maps]) if maps else np.zeros(0, np.int32)
+        with torch.cuda.device(dev), torch.cuda.stream(st):
+            ids = torch.from_numpy(ids_host).to(dev)  # ordered on the copy stream
+            for ev in src.last_events():
+                st.wait_event(ev)
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(st)
+            copied = 0
+            off = 0
+            for what, s_ids, d_ids, s_pool, d_pool, block, group, tail in maps:
+                n = len(s_ids)
+                _lib.check(lib.hy_copy_blocks_tail(
+                    s_pool.data_ptr(), d_pool.data_ptr(), ids.data_ptr() + 4 * off,
+                    ids.data_ptr() + 4 * (off + n), n, block, group, tail, st.cuda_stream),
+                    "hy_copy_blocks_tail")
+                off += 2 * n
+                if what != "last_tok":
+                    copied += copy_bytes(n, block, group, tail)
+            ev1.record(st)
+        dst.launches += len(maps)
+        for rt in (src, dst):
+            rt.wait_before_next_batch(ev1)
+        job._copy = (ev0, ev1, ids)
         self.transfer_stats["count"] += 1
         self.transfer_stats["bytes"] += job.kv_bytes + job.image_bytes
         self.transfer_stats["copied_bytes"] += copied
-        self.transfer_stats["seconds"] += ms * 1e-3
-        self.migration_log.append((job.kind, job.source, job.target, job.rid,
-                                   [(w, list(s), list(d)) for w, s, d, *_ in maps], ms))
+        kind = self.transfer_stats.setdefault(job.kind, {"count": 0, "bytes": 0, "seconds": 0.0})
+        kind["count"] += 1
+        kind["bytes"] += copied
+        self.migration_log.append([job.kind, job.source, job.target, job.rid,
+                                   [(w, list(a), list(b_)) for w, a, b_, *_ in maps
+                                    if w != "last_tok"], None])
+        job._log_entry = self.migration_log[-1]
         # the control message a separate-process target would receive (wire.py, f4)
         iids = list(self.instances)
         msg = MigrationMessage(
             job.kind, job.rid, iids.index(job.source), iids.index(job.target), r.kv_len,
             -1, int(job.kv_bytes + job.image_bytes), self.seed,
-            tuple(BlockMap(w, bb, tuple(s), tuple(d)) for w, s, d, _, _, bb in maps))
+            tuple(BlockMap(w, bb, tuple(a), tuple(b_)) for w, a, b_, _, _, bb, _, _ in maps
+                  if w != "last_tok"))
         self.transfer_stats["control_bytes"] = (self.transfer_stats.get("control_bytes", 0) +
                                                 len(msg.to_bytes()))
         self.last_migration_message = msg
+        if self._live is not None:
+            return 0.0  # provisional: live.py charges the measured time at completion
         if self.clock == "oracle":
             return MG.MigrationJob.transfer_seconds(job, hw)
+        return self._finish_copy(job)
+
+    def copy_done(self, job) -> bool:
+        """True once the job's copy has completed on the device (live mode polls this)."""
+        c = getattr(job, "_copy", None)
+        return c is None or c[1].query()
+
+    def _finish_copy(self, job) -> float:
+        """Wait for the job's copy, record its measured time; returns seconds."""
+        ev0, ev1, _ = job._copy
+        ev1.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        job._copy = None
+        job._seconds = ms * 1e-3
+        job._log_entry[5] = ms
+        self.transfer_stats["seconds"] += ms * 1e-3
+        self.transfer_stats[job.kind]["seconds"] += ms * 1e-3
         return ms * 1e-3
 
     # ------------------------------------------------------------------ results
@@ -246,6 +279,45 @@ class GpuCluster(C.Cluster):
 
     def gpu_launch_count(self) -> int:
         return sum(rt.launches for rt in self.runtimes.values())
+
+
+def copy_bytes(n: int, block: int, group: int, tail: int) -> int:
+    """Bytes ``hy_copy_blocks_tail`` moves for n blocks (the last one token-exact)."""
+    return 0 if n <= 0 else (n - 1) * block + (block // group) * tail
+
+
+def plan_transfer(job, r, shape: MllmShape, src_kv, dst_kv, src_img, dst_img) -> List:
+    """The block copies of one migration job: [(pool, src ids, dst ids, block bytes, group
+    bytes, tail bytes per group)].  KV: the ``kv_blocks_needed(kv_len)`` blocks holding the
+    request's tokens, the last one token-exact; image: the blocks holding its
+    ``visual_tokens`` rows (packed contiguously from its first block), the last one
+    row-exact; PD jobs also carry the 4-byte last sampled token of the request's slot.
+    The copied bytes therefore equal ``job.kv_bytes + job.image_bytes`` (cluster.py:411-413).
+    Pure host logic (CPU-tested)."""
+    out = []
+    if job.kv_bytes > 0:
+        kv_n = MC.kv_blocks_needed(r.kv_len)
+        valid = r.kv_len - (kv_n - 1) * MC.KV_BLOCK_TOKENS
+        grp = MC.KV_BLOCK_TOKENS * shape.head_dim * 2
+        out.append(("kv", list(src_kv.ids[job.rid][:kv_n]), list(dst_kv.ids[job.rid][:kv_n]),
+                    shape.kv_block_elems * 2, grp, valid * shape.head_dim * 2))
+    if job.image_bytes > 0:
+        vt = r.plan.visual_tokens
+        img_n = min(job.image_blocks, MC.image_blocks_needed(vt))
+        blk = shape.image_block_elems * 2
+        valid = vt - (img_n - 1) * MC.IMAGE_BLOCK_TOKENS
+        out.append(("image", list(src_img.ids[job.rid][:img_n]),
+                    list(dst_img.ids[job.rid][:img_n]), blk, blk, valid * shape.hidden * 2))
+    if job.kind == "pd":
+        out.append(("last_tok", [src_kv.slot[job.rid]], [dst_kv.slot[job.rid]], 4, 4, 4))
+    return out
+
+
+def instance_devices(instance_ids: Sequence[str], devices: Sequence) -> Dict[str, "torch.device"]:
+    """Placement: instance k, in the reference's construction order
+    (cluster.py:180-190), runs on devices[k % len(devices)]."""
+    devs = [torch.device(d) for d in devices]
+    return {iid: devs[k % len(devs)] for k, iid in enumerate(instance_ids)}
 
 
 def batch_log_digest(log) -> str:

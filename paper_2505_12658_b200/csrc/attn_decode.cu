@@ -547,13 +547,8 @@ extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads,
                                                      sl2, bps, op, ld_o, part, ns));            \
     break;
   if (G >= 4 && G <= 16 && !getenv("HY_DECODE_GQA_CUDA")) {
-    static bool attr = false;
-    if (!attr) {
-      HY_CUDA_RET(cudaFuncSetAttribute(attn_decode_gqa_mma_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       std::max(GQ_SMEM, (DEC_WARPS * 16 * 130 + 64) * 4)));
-      attr = true;
-    }
+    HY_CUDA_RET(ensure_smem(attn_decode_gqa_mma_kernel,
+                            std::max(GQ_SMEM, (DEC_WARPS * 16 * 130 + 64) * 4)));
     HY_CUDA_RET(launch_pdl(attn_decode_gqa_mma_kernel, dim3(grid), dim3(128),
                            (size_t)std::max(GQ_SMEM, (DEC_WARPS * 16 * 130 + 64) * 4), stream,
                            qp, ld_q, n_kv_heads, G, slots, ctx, block_table, bt_stride, kvp,

@@ -221,12 +221,7 @@ template <int D, bool PAGED>
 static int launch_fa(const FaParams& p, int n_seqs, int n_heads, cudaStream_t st) {
   constexpr int LDS = D + 8;
   constexpr int smem = (64 + 4 * 64) * LDS * 2;
-  static bool attr = false;
-  if (!attr) {
-    HY_CUDA_RET(cudaFuncSetAttribute(attn_fa2_kernel<D, PAGED>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  HY_CUDA_RET(ensure_smem(attn_fa2_kernel<D, PAGED>, smem));
   dim3 grid(n_seqs * p.q_tiles, n_heads);
   HY_CUDA_RET(launch_pdl(attn_fa2_kernel<D, PAGED>, dim3(grid), dim3(128), smem, st, p));
   HY_LAUNCH_CHECK();

@@ -587,12 +587,7 @@ template <int D, bool PAGED, int T>
 static int launch_tc_attn(const CUtensorMap& tq, const CUtensorMap& tkv, const TcAttnParams& p,
                           int n_seqs, int n_heads, cudaStream_t st) {
   using C = TcAttnCfg<D, T>;
-  static bool attr = false;
-  if (!attr) {
-    HY_CUDA_RET(cudaFuncSetAttribute(attn_tc_kernel<D, PAGED, T>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr = true;
-  }
+  HY_CUDA_RET(ensure_smem(attn_tc_kernel<D, PAGED, T>, C::SMEM));
   HY_CUDA_RET(launch_pdl(attn_tc_kernel<D, PAGED, T>, dim3(n_seqs * p.q_tiles, n_heads),
                          dim3(C::THREADS), C::SMEM, st, tq, tkv, p));
   HY_LAUNCH_CHECK();

@@ -436,6 +436,14 @@ int make_tmap_2d_bf16(CUtensorMap* tm, const void* base, uint64_t rows, uint64_t
 
 int num_sms();
 
+// Raise a kernel's dynamic shared-memory limit on the CURRENT device (the attribute is per
+// device; a cache keyed by (device, kernel) under a mutex makes this cheap and thread-safe).
+cudaError_t ensure_smem_attr(const void* kernel, int bytes);
+template <typename... KArgs>
+inline cudaError_t ensure_smem(void (*kernel)(KArgs...), int bytes) {
+  return ensure_smem_attr(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 // kernel-class timer hooks (see hy_set_kernel_timer)
 void timer_mark(int klass, cudaStream_t st, bool begin, double work, long long shape = 0);
 

@@ -321,15 +321,27 @@ __global__ void vit_gather_visual_kernel(const HyImageDesc* __restrict__ images,
 // ---------------------------------------------------------------------------
 __global__ void copy_blocks_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                                    const int* __restrict__ src_ids, const int* __restrict__ dst_ids,
-                                   long long block_bytes) {
+                                   int n, long long block_bytes, int group16, int tail16) {
   pdl_trigger();
   pdl_wait();
   const int b = blockIdx.y;
   const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)src_ids[b] * block_bytes);
   uint4* d = reinterpret_cast<uint4*>(dst + (size_t)dst_ids[b] * block_bytes);
-  const long long n16 = block_bytes / 16;
   const long long stride = (long long)gridDim.x * blockDim.x;
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == n - 1 && tail16 < group16) {
+    // the request's last block: only the first tail16 vectors of every group are valid
+    // (KV: tokens [0, valid) of each [layer][K|V][head] slab; image: the valid rows)
+    const long long groups = (block_bytes / 16) / group16;
+    const long long n16 = groups * tail16;
+    for (; i < n16; i += stride) {
+      const long long g = i / tail16;
+      const long long o = g * group16 + (i - g * tail16);
+      d[o] = ld_nc_v4(s + o);
+    }
+    return;
+  }
+  const long long n16 = block_bytes / 16;
   // 4 independent 16-byte loads in flight per thread
   for (; i + 3 * stride < n16; i += 4 * stride) {
     uint4 a0 = ld_nc_v4(s + i), a1 = ld_nc_v4(s + i + stride), a2 = ld_nc_v4(s + i + 2 * stride),
@@ -340,6 +352,21 @@ __global__ void copy_blocks_kernel(const uint8_t* __restrict__ src, uint8_t* __r
     d[i + 3 * stride] = a3;
   }
   for (; i < n16; i += stride) d[i] = ld_nc_v4(s + i);
+}
+
+// element-granular variant for small records whose size is not a multiple of 16 bytes
+// (the migrated request's last-token slot: 4 bytes)
+__global__ void copy_records_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                    const int* __restrict__ src_ids,
+                                    const int* __restrict__ dst_ids, int n, long long bytes) {
+  pdl_trigger();
+  pdl_wait();
+  const int b = blockIdx.y;
+  const uint8_t* s = src + (size_t)src_ids[b] * bytes;
+  uint8_t* d = dst + (size_t)dst_ids[b] * bytes;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < bytes;
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = s[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -425,21 +452,48 @@ extern "C" int hy_im2col_patches(const HyImageDesc* images, int n_images, int n_
   return 0;
 }
 
-extern "C" int hy_copy_blocks(const void* src_base, void* dst_base, const int* src_ids,
-                              const int* dst_ids, int n, long long block_bytes,
-                              cudaStream_t stream) {
-  HY_CHECK_ARG(block_bytes % 16 == 0, "block_bytes % 16");
+extern "C" int hy_copy_blocks_tail(const void* src_base, void* dst_base, const int* src_ids,
+                                   const int* dst_ids, int n, long long block_bytes,
+                                   long long group_bytes, long long tail_group_bytes,
+                                   cudaStream_t stream) {
+  HY_CHECK_ARG(block_bytes > 0 && n >= 0, "copy shape");
   if (n <= 0) return 0;
+  if (block_bytes % 16 != 0) {  // small unaligned records: whole records only
+    HY_CHECK_ARG(group_bytes == block_bytes && tail_group_bytes == block_bytes,
+                 "tail copies need 16-byte aligned blocks");
+    long long gx = (block_bytes + 255) / 256;
+    dim3 grid((unsigned)(gx < 64 ? gx : 64), n);
+    HY_CUDA_RET(launch_pdl(copy_records_kernel, grid, dim3(256), 0, stream,
+                           reinterpret_cast<const uint8_t*>(src_base),
+                           reinterpret_cast<uint8_t*>(dst_base), src_ids, dst_ids, n,
+                           block_bytes));
+    HY_LAUNCH_CHECK();
+    return 0;
+  }
+  HY_CHECK_ARG(group_bytes > 0 && group_bytes % 16 == 0 && block_bytes % group_bytes == 0,
+               "group_bytes must be a 16-byte multiple dividing block_bytes");
+  HY_CHECK_ARG(tail_group_bytes > 0 && tail_group_bytes % 16 == 0 &&
+                   tail_group_bytes <= group_bytes, "tail_group_bytes in (0, group_bytes], % 16");
+  HY_CHECK_ARG(group_bytes / 16 < (1LL << 31), "group too large");
   long long n16 = block_bytes / 16;
   int threads = 256;
   long long want = (n16 + threads * 4 - 1) / (threads * 4);
   int gx = (int)(want < 256 ? (want < 1 ? 1 : want) : 256);
   dim3 grid(gx, n);
-  HY_CUDA_RET(launch_pdl(copy_blocks_kernel, dim3(grid), dim3(threads), 0, stream, reinterpret_cast<const uint8_t*>(src_base),
-                                                   reinterpret_cast<uint8_t*>(dst_base), src_ids,
-                                                   dst_ids, block_bytes));
+  HY_CUDA_RET(launch_pdl(copy_blocks_kernel, grid, dim3(threads), 0, stream,
+                         reinterpret_cast<const uint8_t*>(src_base),
+                         reinterpret_cast<uint8_t*>(dst_base), src_ids, dst_ids, n, block_bytes,
+                         (int)(group_bytes / 16), (int)(tail_group_bytes / 16)));
   HY_LAUNCH_CHECK();
   return 0;
+}
+
+extern "C" int hy_copy_blocks(const void* src_base, void* dst_base, const int* src_ids,
+                              const int* dst_ids, int n, long long block_bytes,
+                              cudaStream_t stream) {
+  HY_CHECK_ARG(block_bytes % 16 == 0, "block_bytes % 16");
+  return hy_copy_blocks_tail(src_base, dst_base, src_ids, dst_ids, n, block_bytes, block_bytes,
+                             block_bytes, stream);
 }
 
 extern "C" int hy_fill_uniform_bf16(void* dst, long long rows, long long cols, long long ld,

@@ -305,15 +305,54 @@ __device__ __forceinline__ void prefetch_residual(const GemmArgs& a, int m, int 
   }
 }
 
-// stream-K fixup: add up to 3 other contributors' fp32 partials of one 32-column chunk.
-// The first two contributors' loads are all issued before the first add so their L2 round
-// trips overlap (a plain loop serialises one round trip per contributor and chunk; three
-// in flight at once would spill under the 168-register cap).
-__device__ __forceinline__ void add_partials(float* v, const float4* const* srcs, int ns) {
+// stream-K fixup: add up to 3 other contributors' fp32 partials of one 32-column chunk, in
+// the canonical order of the contributors' CTA (pair) index -- a left fold
+// x_c0 + x_c0+1 + ... with this CTA's own accumulators v at position nb -- so the result is
+// bitwise independent of which contributor happens to arrive last (run-to-run
+// deterministic).  srcs[] are the others in CTA order, nb of them before this CTA.  Two
+// contributors' loads are issued before the first add so their L2 round trips overlap
+// (three in flight at once would spill under the register cap).
+__device__ __forceinline__ void add_partials(float* v, const float4* const* srcs, int ns,
+                                             int nb) {
+  float4 f[2][8];
+  int s0 = 0;
+  if (nb > 0) {  // prefix x_c0 + ... + x_(self-1), then + v
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[0][j] = __ldcg(srcs[0] + j * 128);
+    if (nb > 1)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[1][j] = __ldcg(srcs[1] + j * 128);
+    if (nb > 1)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        f[0][j].x += f[1][j].x;
+        f[0][j].y += f[1][j].y;
+        f[0][j].z += f[1][j].z;
+        f[0][j].w += f[1][j].w;
+      }
+    if (nb > 2) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[1][j] = __ldcg(srcs[2] + j * 128);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        f[0][j].x += f[1][j].x;
+        f[0][j].y += f[1][j].y;
+        f[0][j].z += f[1][j].z;
+        f[0][j].w += f[1][j].w;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      v[4 * j] = f[0][j].x + v[4 * j];
+      v[4 * j + 1] = f[0][j].y + v[4 * j + 1];
+      v[4 * j + 2] = f[0][j].z + v[4 * j + 2];
+      v[4 * j + 3] = f[0][j].w + v[4 * j + 3];
+    }
+    s0 = nb;
+  }
 #pragma unroll 1
-  for (int s0 = 0; s0 < ns; s0 += 2) {
+  for (; s0 < ns; s0 += 2) {  // suffix: ((v + x) + y) ...
     const bool two = s0 + 1 < ns;
-    float4 f[2][8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) f[0][j] = __ldcg(srcs[s0] + j * 128);
     if (two)
@@ -321,17 +360,16 @@ __device__ __forceinline__ void add_partials(float* v, const float4* const* srcs
       for (int j = 0; j < 8; ++j) f[1][j] = __ldcg(srcs[s0 + 1] + j * 128);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      float4 g = f[0][j];
+      v[4 * j] += f[0][j].x;
+      v[4 * j + 1] += f[0][j].y;
+      v[4 * j + 2] += f[0][j].z;
+      v[4 * j + 3] += f[0][j].w;
       if (two) {
-        g.x += f[1][j].x;
-        g.y += f[1][j].y;
-        g.z += f[1][j].z;
-        g.w += f[1][j].w;
+        v[4 * j] += f[1][j].x;
+        v[4 * j + 1] += f[1][j].y;
+        v[4 * j + 2] += f[1][j].z;
+        v[4 * j + 3] += f[1][j].w;
       }
-      v[4 * j] += g.x;
-      v[4 * j + 1] += g.y;
-      v[4 * j + 2] += g.z;
-      v[4 * j + 3] += g.w;
     }
   }
 }
@@ -615,15 +653,18 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
           // other contributors' partials (<= 3 by construction of the grid), all loads
           // issued before any add so the L2 round trips overlap
           const float4* srcs[3];
-          int ns = 0;
+          int ns = 0, nb = 0;
           for (int cc = c0; cc <= c1 && ns < 3; ++cc) {
-            if (cc == cta) continue;
+            if (cc == cta) {
+              nb = ns;
+              continue;
+            }
             const long long cu0 = (long long)cc * a.u_sk / G;
             const int slot = cu0 >= ub ? 0 : 1;
             srcs[ns++] = reinterpret_cast<const float4*>(a.partial) +
                          ((size_t)(cc * 2 + slot) * (BN / 32) + c) * 8 * 128 + lrow;
           }
-          add_partials(v, srcs, ns);
+          add_partials(v, srcs, ns, nb);
           epi_chunk<EPI, SWAP>(a, p * 128 + sub * 32, q * BN + c * 32, v, lane,
                                smem_u32(stg_base) + (warp - 2) * kStgBytes, &tmC, nst);
           if (i == 0 && c == 0 && threadIdx.x == 64) HY_TR(11);
@@ -874,15 +915,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
           const float4* srcs[3];
-          int ns = 0;
+          int ns = 0, nb = 0;
           for (int cc = c0; cc <= c1 && ns < 3; ++cc) {
-            if (cc == pair) continue;
+            if (cc == pair) {
+              nb = ns;
+              continue;
+            }
             const long long cu0 = (long long)cc * a.u_sk / npairs;
             const int slot = cu0 >= ub ? 0 : 1;
             srcs[ns++] = reinterpret_cast<const float4*>(a.partial) +
                          (((size_t)(cc * 2 + slot) * 2 + rank) * (BN / 32) + c) * 8 * 128 + lrow;
           }
-          add_partials(v, srcs, ns);
+          add_partials(v, srcs, ns, nb);
           epi_chunk<EPI, false>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32, v, lane,
                                 smem_u32(stg_base) + (warp - 2) * kStgBytes, &tmC, nst);
         }
@@ -911,12 +955,7 @@ template <int BN, int EPI>
 static int launch_pair(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
                        const GemmArgs& a, int grid, cudaStream_t st) {
   using C = GemmPairCfg<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    HY_CUDA_RET(cudaFuncSetAttribute(gemm_pair_kernel<BN, EPI>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
-    attr_set = true;
-  }
+  HY_CUDA_RET(ensure_smem(gemm_pair_kernel<BN, EPI>, C::SMEM_BYTES));
   if (a.dbg & 2)
     gemm_pair_kernel<BN, EPI><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tA, tB, tC, a);
   else
@@ -943,12 +982,7 @@ template <int BN, bool SWAP, int EPI>
 static int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
                        const GemmArgs& a, int grid, cudaStream_t st) {
   using C = GemmCfg<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    HY_CUDA_RET(cudaFuncSetAttribute(gemm_tc_kernel<BN, SWAP, EPI>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES));
-    attr_set = true;
-  }
+  HY_CUDA_RET(ensure_smem(gemm_tc_kernel<BN, SWAP, EPI>, C::SMEM_BYTES));
   HY_CUDA_RET(launch_pdl(gemm_tc_kernel<BN, SWAP, EPI>, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES,
                          st, tA, tB, tC, a));
   HY_LAUNCH_CHECK();

@@ -3,6 +3,7 @@
 #include "../../include/hydra_sm100.h"
 
 #include <atomic>
+#include <map>
 #include <mutex>
 
 namespace hy {
@@ -43,6 +44,20 @@ int num_sms() {
     cached[dev] = n > 0 ? n : 148;
   }
   return cached[dev];
+}
+
+cudaError_t ensure_smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{dev, kernel}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -161,7 +176,11 @@ int side_fork(cudaStream_t st, cudaStream_t* side, cudaEvent_t* join) {
 
 // `waiter` waits for the work enqueued on `from` so far (one extra event per thread)
 int side_mark_and_wait(cudaStream_t from, cudaStream_t waiter) {
-  thread_local cudaEvent_t ev = nullptr;
+  thread_local cudaEvent_t evs[64] = {};
+  int dev = 0;
+  HY_CUDA_RET(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return (int)cudaErrorInvalidDevice;
+  cudaEvent_t& ev = evs[dev];
   if (!ev) HY_CUDA_RET(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   HY_CUDA_RET(cudaEventRecord(ev, from));
   HY_CUDA_RET(cudaStreamWaitEvent(waiter, ev, 0));

@@ -82,7 +82,8 @@ class _Staging:
 
 class InstanceRuntime:
     def __init__(self, inst, shape: MllmShape, weights: DeviceWeights, *, seed: int,
-                 images: ImageStore, resident_inputs: bool = True, max_slots: int = 4096,
+                 images: ImageStore, resident_inputs: bool = True,
+                 max_slots: Optional[int] = None,
                  max_seq_tokens: int = 16384, vit_max_tokens: Optional[int] = None,
                  lang_max_rows: Optional[int] = None, capture: bool = False,
                  pool_bytes_limit: Optional[int] = None):
@@ -104,6 +105,8 @@ class InstanceRuntime:
         if pool_bytes_limit is not None:
             kv_phys = min(kv_cap, pool_bytes_limit // (2 * s.kv_block_elems))
             img_phys = min(img_cap, pool_bytes_limit // (2 * s.image_block_elems))
+        # every concurrent KV holder owns >= 1 block, so capacity bounds the slot count
+        max_slots = max_slots or max(1, min(kv_cap, 32768))
         self.kv_pool = PhysicalCachePool(KVB, kv_cap, max_slots=max_slots,
                                          physical_blocks=kv_phys)
         self.image_pool = PhysicalCachePool(IMG, img_cap, physical_blocks=img_phys)
@@ -128,9 +131,13 @@ class InstanceRuntime:
             self.ev_l = torch.cuda.Event(enable_timing=True)
             self.ev_v = torch.cuda.Event(enable_timing=True)
             self.meta = _Staging(self.device, 1 << 20)
-            self.vmeta = _Staging(self.device, 1 << 16)
-            self.pix = None  # per-batch pixel staging (end-to-end mode)
+            # one metadata / pixel staging pair per vision group of a batch: a group's host
+            # buffer is rewritten only by the next batch, after this batch's events completed
+            self.vmeta_groups: List[_Staging] = []
+            self.pix_groups: List[Optional[_Staging]] = []
             self.tok_log = torch.empty(1 << 20, dtype=torch.int32, device=self.device)
+        self._copy_stream = None
+        self._waits: List = []
         self.kvc = _lib.HyKvCache(self.kv.data_ptr(), s.kv_block_elems, s.kv_layer_elems,
                                   kv_cap, self.block_table.data_ptr(), self.bt_stride)
         self.can_lang = itype.can_prefill or itype.can_decode
@@ -177,12 +184,35 @@ class InstanceRuntime:
             cap = self.lib.hy_lang_workspace_bytes(
                 self.weights.lang, max(rows, self.lang_max_rows), max(n_out, 1024),
                 max(n_dec, 1024), max(max_ctx, self.bt_stride * KVB))
-            self.lang_ws = torch.zeros(max(need, cap), dtype=torch.uint8, device=self.device)
+            # zero-filled on L itself: the forward (and its stream-K arrival counters, which
+            # must start at zero) is stream-ordered after the memset
+            self.lang_ws = None
+            with torch.cuda.stream(self.stream_l):
+                self.lang_ws = torch.zeros(max(need, cap), dtype=torch.uint8,
+                                           device=self.device)
 
     def _ensure_vit_ws(self, tokens: int) -> None:
         need = self.lib.hy_vit_workspace_bytes(self.weights.vit, max(tokens, 1), 0)
         if self.vit_ws is None or self.vit_ws.numel() < need:
-            self.vit_ws = torch.zeros(need, dtype=torch.uint8, device=self.device)
+            # grow geometrically and zero on V, ordered before the ViT forward
+            n = max(need, 2 * self.vit_ws.numel() if self.vit_ws is not None else need)
+            self.vit_ws = None
+            with torch.cuda.stream(self.stream_v):
+                self.vit_ws = torch.zeros(n, dtype=torch.uint8, device=self.device)
+
+    def copy_stream(self):
+        """The stream migrations INTO this instance run on (pull model), created lazily."""
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(self.device)
+        return self._copy_stream
+
+    def last_events(self):
+        """Events that complete with this instance's last launched batch."""
+        return (self.ev_l, self.ev_v)
+
+    def wait_before_next_batch(self, event) -> None:
+        """Order this instance's next batch after ``event`` (a migration copy)."""
+        self._waits.append(event)
 
     def sync_block_tables(self, stream) -> None:
         """Push block lists of requests whose KV allocation changed to the device."""
@@ -207,13 +237,15 @@ class InstanceRuntime:
         val = np.concatenate(val_parts)
         n = idx.size
         buf = torch.from_numpy(np.concatenate([idx, val]))
-        dev = buf.to(self.device, non_blocking=False)
+        # a pageable H2D may return before its DMA lands: issue it on the stream the
+        # scatter runs on, so the scatter is ordered after it
+        with torch.cuda.stream(stream):
+            dev = buf.to(self.device, non_blocking=False)
         _lib.check(self.lib.hy_scatter_i32(self.block_table.data_ptr(), dev.data_ptr(),
                                            dev.data_ptr() + 4 * n, n, stream.cuda_stream),
                    "hy_scatter_i32")
         self.launches += 1
-        torch.cuda.current_stream(self.device).wait_stream(stream)
-        self._keep = dev  # keep alive until the stream consumed it
+        self._keep = dev  # allocated on `stream`: its reuse is ordered after the scatter
 
     # ------------------------------------------------------------------ lowering
     def _lower_language(self, batch, reqs):
@@ -357,6 +389,9 @@ class InstanceRuntime:
         sl, sv = self.stream_l, self.stream_v
         torch.cuda.set_device(dev)
         sl.wait_stream(torch.cuda.current_stream(dev))
+        for ev in self._waits:  # migration copies touching this instance's pools
+            sl.wait_event(ev)
+        self._waits.clear()
         self.ev_start.record(sl)
         sv.wait_event(self.ev_start)
         self.sync_block_tables(sl)
@@ -472,11 +507,14 @@ class InstanceRuntime:
             cur_tok += nt
         if cur:
             groups.append(cur)
-        for g in groups:
-            self._run_vision_group(g, descs, seg, row_maps, sv)
+        while len(self.vmeta_groups) < len(groups):
+            self.vmeta_groups.append(_Staging(self.device, 1 << 16))
+            self.pix_groups.append(None)
+        for gi, g in enumerate(groups):
+            self._run_vision_group(gi, g, descs, seg, row_maps, sv)
         self.stats["images"] += len(descs)
 
-    def _run_vision_group(self, g, descs, seg, row_maps, sv) -> None:
+    def _run_vision_group(self, gi, g, descs, seg, row_maps, sv) -> None:
         s = self.shape
         lib = self.lib
         tok = patch = vis = 0
@@ -501,9 +539,10 @@ class InstanceRuntime:
         else:
             sizes = [gh * gw * s.patch * s.patch * 3 for (_, gh, gw, _, _, _) in recs]
             total = sum((z + 255) & ~255 for z in sizes)
-            if self.pix is None or self.pix.nbytes < total:
-                self.pix = _Staging(self.device, max(total, 1 << 20))
-            hv = self.pix.host.numpy()
+            pix = self.pix_groups[gi]
+            if pix is None or pix.nbytes < total:
+                pix = self.pix_groups[gi] = _Staging(self.device, max(total, 1 << 20))
+            hv = pix.host.numpy()
             off = 0
             offs = []
             for (sidx, gh, gw, _, _, _), z in zip(recs, sizes):
@@ -511,8 +550,8 @@ class InstanceRuntime:
                 offs.append(off)
                 off += (z + 255) & ~255
             with torch.cuda.stream(sv):
-                self.pix.dev[:off].copy_(self.pix.host[:off], non_blocking=True)
-            base = self.pix.dev.data_ptr()
+                pix.dev[:off].copy_(pix.host[:off], non_blocking=True)
+            base = pix.dev.data_ptr()
             for j, ((sidx, gh, gw, t0, p0, v0), o) in enumerate(zip(recs, offs)):
                 arr[j] = _lib.HyImageDesc(base + o, gw * s.patch * 3, gh, gw, t0, p0, v0, 0)
         desc_bytes = np.frombuffer(bytes(arr), dtype=np.uint8)
@@ -521,7 +560,7 @@ class InstanceRuntime:
             "seg": np.asarray([recs[j][3] for j in range(len(recs))] + [tok], dtype=np.int32),
             "rowmap": np.concatenate([row_maps[i] for i in g]),
         }
-        ptrs = self._upload(self.vmeta, parts, sv)
+        ptrs = self._upload(self.vmeta_groups[gi], parts, sv)
         vb = _lib.HyVitBatch(len(g), tok, patch, vis, max_t, ptrs["desc"], ptrs["seg"],
                              ptrs["rowmap"], self.img.data_ptr())
         _lib.check(lib.hy_vit_forward(self.weights.vit, vb, self.vit_ws.data_ptr(),
@@ -529,8 +568,9 @@ class InstanceRuntime:
                    f"hy_vit_forward[{self.iid}]")
 
     def close(self) -> None:
+        self.vmeta_groups, self.pix_groups = [], []
         for name in ("kv", "img", "block_table", "last_tok", "lang_ws", "vit_ws", "tok_log",
-                     "meta", "vmeta", "pix", "_keep"):
+                     "meta", "_keep"):
             if hasattr(self, name):
                 setattr(self, name, None)
         self._img_dev.clear()

@@ -14,8 +14,10 @@ flight in the whole cluster at any moment (the reference's event loop, cluster.p
   is charged to the requests and the reference's own ``_on_batch_done`` runs at the wall
   time of completion, so token timestamps, TTFT and TBT are real;
 * migration control / completion events keep the reference's handlers
-  (``_on_mig_control`` / ``_on_mig_done``); the block copy itself runs when the target
-  reserves the blocks (``GpuMigrationJob``), as in the replay.
+  (``_on_mig_control`` / ``_on_mig_done``); the block copy is launched asynchronously on the
+  target's copy stream when the target reserves the blocks (``GpuMigrationJob``), and
+  ``_on_mig_done`` runs when the copy's completion event fires, charged with the copy's
+  measured device time (the loop never blocks on a copy).
 
 The scheduler, admission, budgets, migration protocol and report are the reference's code,
 unchanged; only the clock and the overlap differ.  One driver thread polls every instance
@@ -42,13 +44,14 @@ def run_live(cluster, trace, *, time_scale: float = 1.0, check_invariants: bool 
         cluster.reqs[req.id] = C.RequestState(spec=req, plan=plan)
         cluster._push(req.arrival_time + plan.preprocess_delay, C._ARRIVAL, req.id)
     cluster._live = {}
+    copies = []  # MIG_DONE events whose copy is still running on the device
     t0 = time.perf_counter()
 
     def now() -> float:
         return (time.perf_counter() - t0) * time_scale
 
     try:
-        while cluster._heap or cluster._live:
+        while cluster._heap or cluster._live or copies:
             progressed = False
             for iid in list(cluster._live):
                 rt = cluster.runtimes[iid]
@@ -66,6 +69,14 @@ def run_live(cluster, trace, *, time_scale: float = 1.0, check_invariants: bool 
                 cluster.now = now()
                 cluster._on_batch_done(iid)
                 progressed = True
+            for rid in list(copies):
+                job = cluster.jobs[rid]
+                if cluster.copy_done(job):
+                    copies.remove(rid)
+                    cluster._finish_copy(job)
+                    cluster.now = now()
+                    cluster._on_mig_done(rid)
+                    progressed = True
             t = now()
             while cluster._heap and cluster._heap[0][0] <= t:
                 _, _, kind, payload = heapq.heappop(cluster._heap)
@@ -75,7 +86,11 @@ def run_live(cluster, trace, *, time_scale: float = 1.0, check_invariants: bool 
                 elif kind == C._MIG_CONTROL:
                     cluster._on_mig_control(payload)
                 elif kind == C._MIG_DONE:
-                    cluster._on_mig_done(payload)
+                    job = cluster.jobs[payload]
+                    if getattr(job, "_copy", None) is not None:
+                        copies.append(payload)  # delivered when the copy completes
+                    else:
+                        cluster._on_mig_done(payload)
                 else:
                     raise AssertionError(f"unexpected event {kind} in live mode")
                 progressed = True

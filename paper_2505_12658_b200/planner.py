@@ -27,17 +27,7 @@ from ._epdsim import EN, MC, E
 TimeFn = Callable[..., float]
 
 
-def _largest_true(lo: int, hi: int, pred) -> int:
-    """Largest n in [lo, hi] with pred(n) for a monotone predicate (engine.py:91-102)."""
-    if pred(hi):
-        return hi
-    while hi - lo > 1:
-        mid = (lo + hi) // 2
-        if pred(mid):
-            lo = mid
-        else:
-            hi = mid
-    return lo
+_largest_true = EN._largest_true  # the reference's own bisection (engine.py:91-102)
 
 
 def measured_stage_budgets(slo, model, hw, summary, t_prefill: TimeFn, t_encode: TimeFn,
@@ -139,3 +129,25 @@ def gpu_stage_timers(runtime, shape, repeats: int = 3):
 def _profiler():
     import epdsim.profiler as P  # the reference package is already on sys.path (._epdsim)
     return P
+
+
+def measured_select_method(trace, N: int, slo, model, hw, goodput_of: Callable,
+                           timers=None):
+    """profiler.select_method (profiler.py:242-270) on measured quantities: Algorithm 2's
+    partition from the measured stage speeds (``timers`` = (t_prefill, t_encode,
+    t_decode); the roofline when None), the three candidate deployments of that partition
+    (``candidate_methods``, profiler.py:180-191), each scored by ``goodput_of(method)`` --
+    on hardware, the replayed goodput of the deployment on N GPUs -- and the argmax with
+    the reference's tie rule (first in candidate order).  Returns the reference's
+    ``SelectionResult``."""
+    P = _profiler()
+    t_prefill, t_encode, t_decode = timers or roofline_timers(model, hw)
+    plan = measured_plan_partition(trace, N, slo, model, hw, t_prefill, t_encode, t_decode)
+    candidates = P.candidate_methods(plan.N_e, plan.N_p, plan.N_d)
+    table = tuple((m, goodput_of(m)) for m in candidates)
+    if all(g == 0.0 for _, g in table):
+        rows = "; ".join(f"{m.label}: goodput 0" for m, _ in table)
+        raise P.ProfilerError(f"all candidate methods infeasible ({rows})")
+    best = max(g for _, g in table)
+    first = next(m for m, g in table if g == best)
+    return P.SelectionResult(best=first, table=table, partition=plan)

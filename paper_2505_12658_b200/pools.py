@@ -46,6 +46,12 @@ class PhysicalCachePool(EN.CachePool):
         return self._allocated
 
     def allocate(self, rid: str, n_blocks: int) -> None:
+        new_holder = n_blocks > 0 and rid not in self.ids
+        if new_holder and self.max_slots and not self._free_slots and self.can_allocate(n_blocks):
+            # checked before any state changes; not a MemoryError, because the reference
+            # would have admitted this request (its pool only counts blocks)
+            raise RuntimeError(f"no free block-table slot for {rid}: {self.max_slots} "
+                               f"concurrent holders (raise max_slots)")
         super().allocate(rid, n_blocks)  # validates, raises MemoryError, updates counts
         if n_blocks == 0:
             return
@@ -54,8 +60,6 @@ class PhysicalCachePool(EN.CachePool):
         if lst is None:
             lst = self.ids[rid] = []
             if self.max_slots:
-                if not self._free_slots:
-                    raise MemoryError(f"no free block-table slot for {rid}")
                 self.slot[rid] = heapq.heappop(self._free_slots)
         pop = heapq.heappop
         free = self._free

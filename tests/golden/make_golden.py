@@ -48,8 +48,10 @@ def write(name, obj):
     print(f"wrote {path}")
 
 
-def config(name, method, model, hw, slo, trace, *, trace_desc, model_desc):
-    spec = ClusterSpec(method=DisaggregationMethod.parse(method))
+def config(name, method, model, hw, slo, trace, *, trace_desc, model_desc, policy=None,
+           spec_overrides=None):
+    spec = ClusterSpec(method=DisaggregationMethod.parse(method),
+                       **({"policy": policy} if policy else {}), **(spec_overrides or {}))
     cap = capture(E, spec, model, hw, slo, trace)
     caps = {}
     for itype, count in spec.method.counts:
@@ -58,6 +60,7 @@ def config(name, method, model, hw, slo, trace, *, trace_desc, model_desc):
             caps[f"{itype.name}{i}"] = [kvb, imb]
     out = {
         "name": name, "method": method, "model": model_desc, "trace": trace_desc,
+        "policy": spec.policy, "spec_overrides": spec_overrides or {},
         "hw": [hw.peak_flops, hw.mem_bandwidth, hw.gpu_memory_bytes, hw.model_weight_bytes,
                hw.interconnect_bandwidth],
         "slo": [slo.ttft_max, slo.tbt_max],
@@ -92,8 +95,35 @@ def main():
     config("qwen_EP1_D1", "EP:1,D:1", qwen, hw_b200(), E.SloSpec(8.0, 0.10), dyn,
            trace_desc="synth_trace(seed=5, n=12, rate=50, images [0,1,2] x [256,576,1024], "
                       "prompt [20,60], output [8,16])", model_desc=QWEN)
-    # known answers from the reference's own tests
+    # baseline scheduling policies (engine.py:406-497): whole-prompt prefills, decodes
+    # first / unbudgeted encodes -- the executor must run their batches too
+    # (a burst -- 32 requests in 0.3 ms -- with budget ceilings of 512 tokens / 2 images, so
+    # the three policies form different batches: stage-level caps encodes at 2 images,
+    # stall-free encodes up to 22 at once, prefill-prioritized runs whole 1242-token prompts)
+    burst = E.scale_to_rate(base, 1e5)
+    tight = {"token_budget_ceiling": 512, "image_budget_ceiling": 2}
+    for pol in ("stage_level", "prefill_prioritized", "stall_free_chunked"):
+        config("config1_burst_" + pol, "EPD:1", tiny, E.DEFAULT_HARDWARE, SLO, burst,
+               policy=pol, spec_overrides=tight, model_desc=TINY,
+               trace_desc="mixed_small.jsonl[:32] scaled to 1e5 req/s; ceilings 512 / 2")
+    # the bench config's model (LLaVA-1.5-7B profile, B200 hardware): decisions of the
+    # full-size model, executed at full width with reduced depth by the GPU parity tests
     llava = E.MODEL_PRESETS["llava-1.5-7b"]
+    cap = E.load_trace(os.path.join(TRACES, "captioning_medium.jsonl"), default_slo=SLO)
+    cap24 = E.scale_to_rate(E.Trace(cap.requests[:24], name="captioning_medium24"), 2000.0)
+    for method in ("EPD:1", "EP:1,D:1"):
+        config("llava_" + method.replace(":", "").replace(",", "_"), method, llava, hw_b200(),
+               SLO, cap24, trace_desc="captioning_medium.jsonl[:24] scaled to 2000 req/s",
+               model_desc="llava-1.5-7b")
+    # multi-image high-resolution stress (BASELINE config 5 shape, workload.py:234-264):
+    # 4 images x ~2.9k tokens, prompts 1-2k, contexts to ~14k tokens, PD jobs of ~870 blocks
+    stress = E.synth_trace(seed=21, n_requests=3, rate=2.0, image_count_dist=4,
+                           visual_token_choices=[2800, 2900, 3000], prompt_dist=[1000, 2000],
+                           output_dist=[64, 128], slo=SLO)
+    config("llava_stress_EP1_D1", "EP:1,D:1", llava, hw_b200(), SLO, stress,
+           trace_desc="synth_trace(seed=21, n=3, rate=2, 4 images x [2800,2900,3000], "
+                      "prompt [1000,2000], output [64,128])", model_desc="llava-1.5-7b")
+    # known answers from the reference's own tests
     ka = {
         "llava_kv_bytes_per_token": llava.kv_bytes_per_token,           # test_model_cost.py:197
         "llava_image_bytes_576": E.image_cache_bytes(576, llava),         # test_migration.py:28-30

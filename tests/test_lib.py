@@ -43,3 +43,18 @@ def test_library_is_sm100a():
                           text=True).stdout
     # tcgen05 MMA + TMA loads + TMEM loads prove the Blackwell-native GEMM path
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+
+
+def test_host_modules_do_not_map_the_library():
+    """The reference arm of bench.py (epdsim + the CPU port) imports the package's host
+    modules; the .so must only load on first device use (GpuCluster / InstanceRuntime /
+    DeviceWeights), so that arm never maps it."""
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import paper_2505_12658_b200 as P\n"
+            "from paper_2505_12658_b200 import _lib, inputs, shapes, planner, weights\n"
+            "import oracle.cpu_executor, bench\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "assert _lib._lib is None and 'libhydra_sm100' not in maps\n"
+            "print('ok')\n") % ROOT
+    out = subprocess.run(["python", "-c", code], capture_output=True, text=True, cwd=ROOT)
+    assert out.stdout.strip() == "ok", out.stderr

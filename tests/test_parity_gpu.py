@@ -14,6 +14,7 @@ Several instances share one GPU here (gpurun gives one GPU); cross-GPU copies us
 same kernel through peer pointers.
 """
 
+import numpy as np
 import pytest
 import torch
 
@@ -21,14 +22,20 @@ from oracle.batch_log import block_maps
 from paper_2505_12658_b200 import get_shape, with_layers
 from paper_2505_12658_b200._epdsim import C, E
 from paper_2505_12658_b200.cluster import GpuCluster, batch_log_digest
-from parity_util import LOGIT_ATOL, golden_trace, load_golden, normalise, oracle_replay
+from parity_util import (LOGIT_ATOL, LOGIT_MEAN_RTOL, LOGIT_RTOL, golden_trace, load_golden, normalise,
+                         oracle_replay)
 
 pytestmark = pytest.mark.gpu
 
 
+def _spec(g):
+    return C.ClusterSpec(method=C.DisaggregationMethod.parse(g["method"]),
+                         policy=g.get("policy", "stage_level"), **g.get("spec_overrides", {}))
+
+
 def _run(name, shape, **kw):
     g = load_golden(name)
-    spec = C.ClusterSpec(method=C.DisaggregationMethod.parse(g["method"]))
+    spec = _spec(g)
     cl = GpuCluster(spec, shape, E.HardwareProfile(*g["hw"]), E.SloSpec(*g["slo"]),
                     clock="oracle", record_batches=True, capture=True,
                     pool_bytes_limit=4 << 30, **kw)
@@ -84,9 +91,17 @@ def _check_device_tables(cl):
             assert bt[s, :len(ids)].tolist() == ids
 
 
-@pytest.mark.parametrize("name", ["config1_2000rps", "tiny_EP1_D1", "tiny_E1_P1_D1",
-                                  "tiny_E1_PD1"])
+@pytest.mark.parametrize("name", ["config1_2000rps", "config1_native", "tiny_EP1_D1",
+                                  "tiny_E1_P1_D1", "tiny_E1_PD1",
+                                  "config1_burst_stage_level",
+                                  "config1_burst_prefill_prioritized",
+                                  "config1_burst_stall_free_chunked"])
 def test_tiny_cluster_parity(name):
+    """Tiny model (BASELINE config 1): the native-rate golden log whose sha BASELINE.md
+    records, the 2000 req/s replay, three disaggregations, and a burst under the three
+    scheduling policies (engine.py:333-497: stage-level, whole-prompt prefill-prioritized,
+    and stall-free with unbudgeted encodes -- up to 22 images in one encode batch, split
+    into several ViT groups)."""
     shape = get_shape("tiny")
     g, cl, alloc_log = _run(name, shape)
     assert batch_log_digest(cl.batch_log) == g["sha"]
@@ -95,7 +110,10 @@ def test_tiny_cluster_parity(name):
     _check_blocks(g, cl, alloc_log)
     _check_device_tables(cl)
     res = oracle_replay(cl, shape, seed=0)
+    print(name, {k: v for k, v in res.items() if k != "near_tie_list"},
+          "near-ties (iid, batch, rid, oracle gap):", res["near_tie_list"])
     assert res["max_abs_err"] <= LOGIT_ATOL, res
+    assert not res["violations"], res
     assert res["tokens_equal"] + res["near_ties"] == res["rows"], res
     assert res["near_ties"] <= 0.05 * res["rows"], res
     # every request produced exactly output_tokens tokens
@@ -110,6 +128,53 @@ def test_tiny_cluster_parity(name):
         assert [(m.pool, list(m.src_ids), list(m.dst_ids)) for m in msg.maps] == maps
 
 
+@pytest.mark.parametrize("name", ["llava_EPD1", "llava_EP1_D1", "llava_stress_EP1_D1"])
+def test_llava_full_width_parity(name):
+    """The bench config's model: LLaVA-1.5-7B at full width (ViT 1024/16 heads, decoder
+    4096/32 heads, vocab 32000) with depth 2+2 so the fp32 CPU oracle stays tractable;
+    scheduler decisions are the full 32+24-layer model's (golden from the reference with
+    the llava-1.5-7b preset on a B200 HardwareProfile).  Covers colocated EPD:1, the
+    2-instance EP:1,D:1 split (24 PD migrations of up to 39 blocks), and the multi-image
+    stress shape (4 images x ~2.9k tokens per request, 13.6k-token prefill chunks,
+    ~850-block PD migrations)."""
+    full = get_shape("llava-1.5-7b")
+    shape = with_layers(full, n_layers=2, v_layers=2)
+    g, cl, alloc_log = _run(name, shape, profile_override=full.profile())
+    assert batch_log_digest(cl.batch_log) == g["sha"]
+    assert normalise(cl.batch_log) == g["batches"]
+    assert len(cl.migration_log) == len(g["migrations"])
+    _check_blocks(g, cl, alloc_log)
+    _check_device_tables(cl)
+    res = oracle_replay(cl, shape, seed=0, rtol=LOGIT_RTOL)
+    print(name, {k: v for k, v in res.items() if k != "near_tie_list"},
+          "near-ties (iid, batch, rid, oracle gap):", res["near_tie_list"])
+    assert res["max_rel_err"] <= LOGIT_RTOL and not res["violations"], res
+    assert res["mean_rel_err"] <= LOGIT_MEAN_RTOL, res
+    assert res["tokens_equal"] + res["near_ties"] == res["rows"], res
+    # random-init logits are nearly flat (expected top-2 gap ~0.3 at rms 1.3), so a few
+    # percent of greedy picks are near-ties; every one is listed in the output above
+    assert res["near_ties"] <= 0.08 * res["rows"], res
+    for rid, toks in cl.generated.items():
+        assert len(toks) == cl.reqs[rid].spec.output_tokens
+
+
+def test_gpu_path_is_deterministic():
+    """Two replays of the same inputs give bitwise-identical logits and tokens (stream-K
+    partials are summed in contributor order, not arrival order)."""
+    shape = get_shape("tiny")
+    logs = []
+    for _ in range(2):
+        g, cl, _ = _run("config1_2000rps", shape)
+        logs.append([cl.runtimes[iid].exec_log[idx] for iid, idx in cl.exec_order])
+    a, b = logs
+    assert len(a) == len(b)
+    for x, y in zip(a, b):
+        assert x["out_rids"] == y["out_rids"]
+        if "logits" in x:
+            assert np.array_equal(x["logits"], y["logits"])
+            assert np.array_equal(x["tokens"], y["tokens"])
+
+
 def test_qwen_shaped_hybrid_ep_d_parity():
     """Config 3 shape class (GQA 7, head_dim 80 ViT, 2x2 merger, qkv bias, dynamic
     resolution) with the depth reduced so the fp32 CPU oracle stays fast; decisions use
@@ -117,18 +182,21 @@ def test_qwen_shaped_hybrid_ep_d_parity():
     full = get_shape("qwen2-vl-7b")
     shape = with_layers(full, n_layers=2, v_layers=2)
     g = load_golden("qwen_EP1_D1")
-    spec = C.ClusterSpec(method=C.DisaggregationMethod.parse(g["method"]))
+    spec = _spec(g)
     prof = E.ModelProfile(**g["model"])
-    cl =GpuCluster(spec, shape, E.HardwareProfile(*g["hw"]), E.SloSpec(*g["slo"]),
+    cl = GpuCluster(spec, shape, E.HardwareProfile(*g["hw"]), E.SloSpec(*g["slo"]),
                     clock="oracle", record_batches=True, capture=True, pool_bytes_limit=4 << 30,
                     profile_override=prof)
     cl.run(golden_trace(E, g), check_invariants=True)
     assert batch_log_digest(cl.batch_log) == g["sha"]
     _check_device_tables(cl)
-    res = oracle_replay(cl, shape, seed=0)
-    # Qwen2-shaped logits are ~3x larger (hidden 3584, 152k vocab) than the tiny model's;
-    # the bound scales with them (measured 0.072 with all 128 greedy ids equal)
-    assert res["max_abs_err"] <= 5 * LOGIT_ATOL, res
+    res = oracle_replay(cl, shape, seed=0, rtol=LOGIT_RTOL)
+    print("qwen", {k: v for k, v in res.items() if k != "near_tie_list"},
+          "near-ties:", res["near_tie_list"])
+    # Qwen2-shaped logits are larger (hidden 3584, 152k vocab) than the tiny model's: the
+    # bound is the same one stated relative to the logit scale (parity_util.LOGIT_RTOL)
+    assert res["max_rel_err"] <= LOGIT_RTOL and not res["violations"], res
+    assert res["mean_rel_err"] <= LOGIT_MEAN_RTOL, res
     assert res["tokens_equal"] + res["near_ties"] == res["rows"], res
 
 

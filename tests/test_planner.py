@@ -47,3 +47,25 @@ def test_slower_decode_shifts_instances_to_decode():
                                    lambda n, ctx: 3.0 * td(n, ctx))
     assert slow.N_d >= base.N_d and slow.t_d > base.t_d
     assert base.N_e + base.N_p + base.N_d == 8 == slow.N_e + slow.N_p + slow.N_d
+
+
+@pytest.mark.parametrize("N", [3, 4])
+def test_measured_selection_reproduces_reference_select_method(N):
+    """f3 (profiler.py:216-270): with roofline timers and the reference's own replayed
+    goodput as the scorer, measured_select_method picks exactly what select_method picks
+    (same partition, same three candidates, same goodput table, same tie rule)."""
+    from paper_2505_12658_b200.planner import measured_select_method
+    model = get_shape("llava-1.5-7b").profile()
+    hw = b200_hardware()
+    slo = E.SloSpec(4.0, 0.08)
+    tr = E.synth_trace(seed=7, n_requests=60, rate=4.0, image_count_dist=1,
+                       visual_token_choices=576, prompt_dist=[25, 35, 45],
+                       output_dist=[90, 110, 130], slo=slo)
+    bounds = (1.0, 64.0)
+    ref = P.select_method(tr, N, slo, model, hw, rate_bounds=bounds, tolerance=0.5)
+    got = measured_select_method(
+        tr, N, slo, model, hw,
+        lambda m: P.method_goodput(m, tr, slo, model, hw, bounds, 0.5))
+    assert got.best == ref.best
+    assert got.table == ref.table
+    assert got.partition == ref.partition
