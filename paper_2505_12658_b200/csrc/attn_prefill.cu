@@ -236,10 +236,11 @@ int attn_tc_varlen(const void* qkv, int ld_qkv, int n_rows, int n_segs, const in
                    int max_len, int n_heads, int head_dim, float scale, void* out, int ld_o,
                    cudaStream_t st);
 
-// tcgen05 kernel for head_dim 64/128 unless HY_ATTN_FA2 is set (A/B measurement only)
-static bool use_tc(int head_dim) {
+// tcgen05 kernel for head_dim 64/128 (and 80 for the varlen ViT path) unless HY_ATTN_FA2 is
+// set (A/B measurement only)
+static bool use_tc(int head_dim, bool varlen = false) {
   static const bool fa2 = getenv("HY_ATTN_FA2") != nullptr;
-  return !fa2 && (head_dim == 64 || head_dim == 128);
+  return !fa2 && (head_dim == 64 || head_dim == 128 || (varlen && head_dim == 80));
 }
 
 }  // namespace hy
@@ -287,7 +288,7 @@ extern "C" int hy_attn_varlen(const void* qkv, int ld_qkv, int n_rows, int n_seg
                               int max_len, int n_heads, int head_dim, float scale, void* out,
                               int ld_o, cudaStream_t stream) {
   if (n_segs <= 0 || max_len <= 0 || n_rows <= 0) return 0;
-  if (use_tc(head_dim))
+  if (use_tc(head_dim, true))
     return attn_tc_varlen(qkv, ld_qkv, n_rows, n_segs, seg, max_len, n_heads, head_dim, scale,
                           out, ld_o, stream);
   FaParams p{};

@@ -16,8 +16,10 @@
 //               only when a row max grows by more than 2^8 -- P stays <= 256, exact in the
 //               final O / l.  Finally O / l -> bf16 -> global.
 //
-// Same math as the mma.sync kernel it replaces for d in {64, 128} (attn_prefill.cu keeps
-// that kernel for other head sizes, e.g. Qwen2-VL's d = 80 vision tower).
+// Same math as the mma.sync kernel it replaces, for d in {64, 128}, and d = 80 (Qwen2-VL's
+// vision tower) as zero-padded d = 128 tiles (the softmax-bound kernel has tensor-pipe
+// headroom for the 1.6x MMA work; attn_prefill.cu's mma.sync kernel is now only the
+// HY_ATTN_FA2 A/B reference).
 // Reference: epdsim prices prefill attention as 4 S^2 H per chunk (model_cost.py:189) and
 // ViT attention as 4 T^2 H_v per image (model_cost.py:160-163).
 #include "common.cuh"
@@ -105,7 +107,10 @@ struct TcAttnCfg {
   static constexpr int THREADS = 64 + 256;
 };
 
-template <int D, bool PAGED, int T>
+// DV: the real head dim when it is narrower than the D-wide tiles (varlen only): Q/K/V are
+// fetched through a 3D map [rows][heads][DV] whose boxes past DV are zero-filled, so the
+// padded dims add nothing to S and leave O's extra columns zero; only DV columns are stored.
+template <int D, bool PAGED, int T, int DV = D>
 __global__ void __launch_bounds__(64 + 256, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                    const TcAttnParams p) {
@@ -171,9 +176,14 @@ __global__ void __launch_bounds__(64 + 256, 1)
     if (lane == 0) {
       mbar_expect_tx(q_full, C::TILES * C::Q_BYTES);
       for (int t = 0; t < C::TILES; ++t)
-        for (int c = 0; c < C::NC; ++c)
-          tma_load_2d(&tmQ, q_full, sQ + t * C::Q_BYTES + c * C::CHUNK, h * D + c * 64,
-                      q0 + qbase + t * C::BQ, kEvictFirst);
+        for (int c = 0; c < C::NC; ++c) {
+          if (DV != D)
+            tma_load_3d(&tmQ, q_full, sQ + t * C::Q_BYTES + c * C::CHUNK, c * 64, h,
+                        q0 + qbase + t * C::BQ, kEvictFirst);
+          else
+            tma_load_2d(&tmQ, q_full, sQ + t * C::Q_BYTES + c * C::CHUNK, h * D + c * 64,
+                        q0 + qbase + t * C::BQ, kEvictFirst);
+        }
     }
     constexpr int BPT = C::BK / HY_KV_BLOCK_TOKENS;  // cache blocks per key tile (8)
     const int* bt = PAGED ? p.block_table + (size_t)p.slots[seq] * p.bt_stride : nullptr;
@@ -205,9 +215,14 @@ __global__ void __launch_bounds__(64 + 256, 1)
                         kEvictNormal);
       } else if (lane == 0) {
 #pragma unroll
-        for (int c = 0; c < C::NC; ++c)
-          tma_load_2d(&tmKV, &k_full[st], sK + c * C::CHUNK, p.k_col0 + kvh * D + c * 64,
-                      q0 + j * C::BK, kEvictNormal);
+        for (int c = 0; c < C::NC; ++c) {
+          if (DV != D)  // k_col0 is a head index here
+            tma_load_3d(&tmKV, &k_full[st], sK + c * C::CHUNK, c * 64, p.k_col0 + kvh,
+                        q0 + j * C::BK, kEvictNormal);
+          else
+            tma_load_2d(&tmKV, &k_full[st], sK + c * C::CHUNK, p.k_col0 + kvh * D + c * 64,
+                        q0 + j * C::BK, kEvictNormal);
+        }
       }
       // V_j
       if (lane == 0) {
@@ -223,9 +238,14 @@ __global__ void __launch_bounds__(64 + 256, 1)
                         (int)(row + p.rows_per_kv), kEvictNormal);
       } else if (lane == 0) {
 #pragma unroll
-        for (int c = 0; c < C::NC; ++c)
-          tma_load_2d(&tmKV, &v_full[st], sV + c * C::CHUNK, p.v_col0 + kvh * D + c * 64,
-                      q0 + j * C::BK, kEvictNormal);
+        for (int c = 0; c < C::NC; ++c) {
+          if (DV != D)
+            tma_load_3d(&tmKV, &v_full[st], sV + c * C::CHUNK, c * 64, p.v_col0 + kvh,
+                        q0 + j * C::BK, kEvictNormal);
+          else
+            tma_load_2d(&tmKV, &v_full[st], sV + c * C::CHUNK, p.v_col0 + kvh * D + c * 64,
+                        q0 + j * C::BK, kEvictNormal);
+        }
       }
       // warm L2 with the next tile's blocks: its TMA loads (issued once a stage frees up)
       // then hit L2 instead of HBM -- the 32 small boxes per tile are latency-bound
@@ -386,7 +406,7 @@ __global__ void __launch_bounds__(64 + 256, 1)
           l *= f;
           if (need) m_used = m_new;
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
+          for (int c = 0; c < (DV + 31) / 32; ++c) {
             uint32_t o[32];
             tmem_ld_32x32b_x32(tO + c * 32, o);
             tmem_ld_wait();
@@ -438,14 +458,15 @@ __global__ void __launch_bounds__(64 + 256, 1)
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < (DV + 31) / 32; ++c) {
       uint32_t o[32];
       tmem_ld_32x32b_x32(tO + c * 32, o);
       tmem_ld_wait();
       if (qrow < nq) {
-        bf16* dst = p.out + (size_t)(q0 + qrow) * p.ld_o + (size_t)h * D + c * 32;
+        bf16* dst = p.out + (size_t)(q0 + qrow) * p.ld_o + (size_t)h * DV + c * 32;
 #pragma unroll
         for (int u = 0; u < 32; u += 8) {
+          if (c * 32 + u >= DV) break;
           float v[8];
 #pragma unroll
           for (int w = 0; w < 8; ++w) v[w] = __uint_as_float(o[u + w]) * inv;
@@ -559,13 +580,15 @@ __global__ void __launch_bounds__(64 + 256, 1)
     const float inv = lt > 0.f ? 1.f / lt : 0.f;
 #pragma unroll 1
     for (int c = 0; c < D / 64; ++c) {
+      if (hc * (D / 2) + c * 32 >= DV) break;
       uint32_t o[32];
       tmem_ld_32x32b_x32(tO + c * 32, o);
       tmem_ld_wait();
       if (qrow < nq) {
-        bf16* dst = p.out + (size_t)(q0 + qrow) * p.ld_o + (size_t)h * D + hc * (D / 2) + c * 32;
+        bf16* dst = p.out + (size_t)(q0 + qrow) * p.ld_o + (size_t)h * DV + hc * (D / 2) + c * 32;
 #pragma unroll
         for (int u = 0; u < 32; u += 8) {
+          if (hc * (D / 2) + c * 32 + u >= DV) break;
           float v[8];
 #pragma unroll
           for (int w = 0; w < 8; ++w) v[w] = __uint_as_float(o[u + w]) * inv;
@@ -583,12 +606,12 @@ __global__ void __launch_bounds__(64 + 256, 1)
   }
 }
 
-template <int D, bool PAGED, int T>
+template <int D, bool PAGED, int T, int DV = D>
 static int launch_tc_attn(const CUtensorMap& tq, const CUtensorMap& tkv, const TcAttnParams& p,
                           int n_seqs, int n_heads, cudaStream_t st) {
   using C = TcAttnCfg<D, T>;
-  HY_CUDA_RET(ensure_smem(attn_tc_kernel<D, PAGED, T>, C::SMEM));
-  HY_CUDA_RET(launch_pdl(attn_tc_kernel<D, PAGED, T>, dim3(n_seqs * p.q_tiles, n_heads),
+  HY_CUDA_RET(ensure_smem(attn_tc_kernel<D, PAGED, T, DV>, C::SMEM));
+  HY_CUDA_RET(launch_pdl(attn_tc_kernel<D, PAGED, T, DV>, dim3(n_seqs * p.q_tiles, n_heads),
                          dim3(C::THREADS), C::SMEM, st, tq, tkv, p));
   HY_LAUNCH_CHECK();
   return 0;
@@ -644,7 +667,8 @@ int attn_tc_prefill(const void* q, int ld_q, int n_rows, int n_seqs, const int* 
 int attn_tc_varlen(const void* qkv, int ld_qkv, int n_rows, int n_segs, const int* seg,
                    int max_len, int n_heads, int head_dim, float scale, void* out, int ld_o,
                    cudaStream_t st) {
-  HY_CHECK_ARG(head_dim == 128 || head_dim == 64, "tcgen05 attention: head_dim 64 or 128");
+  HY_CHECK_ARG(head_dim == 128 || head_dim == 64 || head_dim == 80,
+               "tcgen05 attention: head_dim 64, 80 or 128");
   TcAttnParams p{};
   p.qstart = seg;
   const int T = attn_tiles(n_segs, max_len, n_heads);
@@ -656,6 +680,17 @@ int attn_tc_varlen(const void* qkv, int ld_qkv, int n_rows, int n_segs, const in
   p.out = reinterpret_cast<bf16*>(out);
   p.ld_o = ld_o;
   CUtensorMap tm;
+  if (head_dim == 80) {
+    // Qwen2-VL's vision tower: each head's 80 dims padded to 128 by the TMA's out-of-bounds
+    // zero fill (3D map [rows][3 * heads][80]); the tile math is the d = 128 kernel's
+    HY_CHECK_ARG((ld_qkv * 2) % 16 == 0, "ld_qkv");
+    p.k_col0 = n_heads;  // head indices in the 3D map
+    p.v_col0 = 2 * n_heads;
+    HY_RET_IF(make_tmap_3d_bf16(&tm, qkv, 80, (uint64_t)3 * n_heads, n_rows, 80 * 2,
+                                (uint64_t)ld_qkv * 2, 64, 128));
+    return T == 2 ? launch_tc_attn<128, false, 2, 80>(tm, tm, p, n_segs, n_heads, st)
+                  : launch_tc_attn<128, false, 1, 80>(tm, tm, p, n_segs, n_heads, st);
+  }
   HY_RET_IF(make_tmap_2d_bf16(&tm, qkv, n_rows, (uint64_t)3 * n_heads * head_dim,
                               (uint64_t)ld_qkv * 2, 128, 64));
   if (T == 2)

@@ -209,6 +209,16 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* tm, uint64_t* bar
       : "memory");
 }
 
+// 3D tiled TMA load (box coordinates c0 innermost).
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* tm, uint64_t* bar, void* dst,
+                                            int c0, int c1, int c2, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::"
+      "cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(cache_hint)
+      : "memory");
+}
+
 // Prefetch a 2D TMA box into L2 (no shared-memory destination, no completion tracking).
 // TMA store shared -> global (bulk-group completion) and its group waits
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, uint32_t src, int c0, int c1) {
@@ -433,6 +443,12 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
 int make_tmap_2d_bf16(CUtensorMap* tm, const void* base, uint64_t rows, uint64_t cols,
                       uint64_t row_stride_bytes, uint32_t box_rows, uint32_t box_cols,
                       int swizzle = 3);
+
+// 3D bf16 map: dims {d0 (contiguous), d1, d2} with byte strides s1 (dim 1), s2 (dim 2); box
+// {b0, 1, b2}.  Boxes reaching past d0 are zero-filled by the TMA unit (used to pad a head
+// dim of 80 to the 128-wide tcgen05 attention tiles).
+int make_tmap_3d_bf16(CUtensorMap* tm, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                      uint64_t s1, uint64_t s2, uint32_t b0, uint32_t b2, int swizzle = 3);
 
 int num_sms();
 

@@ -257,7 +257,7 @@ def test_prefill_attention_paged(n_heads, n_kv, chunks, tiles, monkeypatch):
 
 @pytest.mark.parametrize("tiles", ["1", "2"])  # query tiles per CTA of the tcgen05 kernel
 @pytest.mark.parametrize("d,lens", [(64, [577, 577, 10]), (80, [1024, 64, 300]), (128, [65]),
-                                    (128, [300, 129, 1])])
+                                    (128, [300, 129, 1]), (64, [2901, 1]), (80, [4, 2304])])
 def test_vit_varlen_attention(d, lens, tiles, monkeypatch):
     monkeypatch.setenv("HY_ATTN_T", tiles)
     nh = 4
@@ -351,6 +351,29 @@ def test_copy_blocks_and_scatter_bit_exact():
     val = torch.tensor([1, 2, 3], dtype=torch.int32, device=DEV)
     ck(lib().hy_scatter_i32(t.data_ptr(), idx.data_ptr(), val.data_ptr(), 3, st()))
     assert t[5].item() == 1 and t[99].item() == 2 and t[0].item() == 3
+
+
+@pytest.mark.parametrize("block,group,tail", [(4096 * 6, 4096, 7 * 256), (4096 * 6, 4096, 4096),
+                                              (576 * 64, 576 * 64, 100 * 64), (4, 4, 4)])
+def test_copy_blocks_tail_token_exact(block, group, tail):
+    """hy_copy_blocks_tail: whole blocks except the last, whose groups copy only their first
+    `tail` bytes (KV: valid tokens of each [layer][K|V][head] slab); nothing else written."""
+    nb = 12
+    src = torch.randint(1, 255, (nb, block), dtype=torch.uint8, device=DEV)
+    dst = torch.zeros(nb, block, dtype=torch.uint8, device=DEV)
+    s_ids = torch.tensor([3, 7, 0, 11], dtype=torch.int32, device=DEV)
+    d_ids = torch.tensor([0, 1, 5, 2], dtype=torch.int32, device=DEV)
+    ck(lib().hy_copy_blocks_tail(src.data_ptr(), dst.data_ptr(), s_ids.data_ptr(),
+                                 d_ids.data_ptr(), 4, block, group, tail, st()))
+    torch.cuda.synchronize()
+    for s_, d_ in zip(s_ids.tolist()[:-1], d_ids.tolist()[:-1]):
+        assert torch.equal(dst[d_], src[s_])
+    last_s, last_d = s_ids.tolist()[-1], d_ids.tolist()[-1]
+    want = torch.zeros(block, dtype=torch.uint8, device=DEV).view(-1, group)
+    want[:, :tail] = src[last_s].view(-1, group)[:, :tail]
+    assert torch.equal(dst[last_d], want.view(-1))
+    untouched = [i for i in range(nb) if i not in d_ids.tolist()]
+    assert int(dst[untouched].sum()) == 0
 
 
 def test_merge_embed_bit_exact():
