@@ -75,6 +75,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=3,
                     help="requests of the trace the CPU port replays per step")
+    ap.add_argument("--trace", default="textcaps", choices=sorted(TRACES))
+    ap.add_argument("--emulate-link-gbs", type=float, default=770.0,
+                    help="with co-located GPU slots (--devices 0,0,...), charge each migration "
+                         "max(measured copy, bytes / this link bandwidth) (measured NVLink peer "
+                         "copy, B200_PROFILING.md)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--budgets", default="measured", choices=["measured", "roofline"],
                     help="per-batch token/image budgets: reference search over GPU-timed "
@@ -96,11 +101,30 @@ def measured_peaks():
                 "sm_max_mhz": 1965.0}, "fallback"
 
 
-def base_trace(E, n, seed=7):
-    slo = E.SloSpec(4.0, 0.08)
-    return E.synth_trace(seed=seed, n_requests=n, rate=1.0, image_count_dist=1,
-                         visual_token_choices=576, prompt_dist=[25, 35, 45],
-                         output_dist=[90, 110, 130], slo=slo, name="textcaps_synth"), slo
+TRACES = {
+    # BASELINE configs 2 / 4: TextCaps-shaped, one 576-token image (LLaVA)
+    "textcaps": dict(seed=7, image_count_dist=1, visual_token_choices=576,
+                     prompt_dist=[25, 35, 45], output_dist=[90, 110, 130], slo=(4.0, 0.08),
+                     desc="TextCaps-shaped synth_trace(seed=7): 1 image x 576 tokens, "
+                          "prompt {25,35,45}, output {90,110,130}; SLO TTFT 4 s / TBT 0.08 s"),
+    # BASELINE config 3: dynamic-resolution images (Qwen2-VL), SLO qwen2-vl-7b/textcaps
+    "dynres": dict(seed=11, image_count_dist=1, visual_token_choices=[256, 576, 1024, 1600, 2916],
+                   prompt_dist=[25, 35, 45], output_dist=[90, 110, 130], slo=(8.0, 0.10),
+                   desc="dynamic-resolution synth_trace(seed=11): 1 image x {256,576,1024,1600,"
+                        "2916} tokens, prompt {25,35,45}, output {90,110,130}; SLO TTFT 8 s / "
+                        "TBT 0.10 s (presets.py:55)"),
+}
+TRACE = "textcaps"
+
+
+def base_trace(E, n, seed=None):
+    t = TRACES[TRACE]
+    slo = E.SloSpec(*t["slo"])
+    return E.synth_trace(seed=t["seed"] if seed is None else seed, n_requests=n, rate=1.0,
+                         image_count_dist=t["image_count_dist"],
+                         visual_token_choices=t["visual_token_choices"],
+                         prompt_dist=t["prompt_dist"], output_dist=t["output_dist"], slo=slo,
+                         name=TRACE), slo
 
 
 def n_gpus(args, d) -> int:
@@ -114,10 +138,10 @@ def method_for(args, n: int) -> str:
 def workload_config(args, n: int) -> dict:
     """The workload both arms run (identical dict in both JSON lines)."""
     method = method_for(args, n)
-    return {"workload": f"{args.model} shape, {method} on {n} GPU(s), TextCaps-shaped "
-                        "synth_trace(seed=7): 1 image x 576 tokens, prompt {25,35,45}, "
-                        "output {90,110,130}; SLO TTFT 4 s / TBT 0.08 s (P90 attainment)",
-            "model": args.model, "method": method, "requests": args.requests * n,
+    return {"workload": f"{args.model} shape, {method} on {n} GPU(s), "
+                        f"{TRACES[args.trace]['desc']} (P90 attainment)",
+            "model": args.model, "method": method, "trace": args.trace,
+            "requests": args.requests * n,
             "requests_per_gpu": args.requests,
             "rate_bounds_per_gpu": [args.rate_lo, args.rate_hi],
             "parallelism": (f"disaggregated {method}: one instance per GPU, EP/PD migrations "
@@ -265,6 +289,7 @@ def run_ours(args, d: Dist):
     # co-located instances (repeated --devices entries) split the device's pool memory
     share = max(idx.count(i) for i in phys)
     pool_limit = None if share == 1 else int(120e9 / share)
+    emulated = share > 1 and n > 1  # several GPU slots on one device (see GpuCluster)
     base, slo = base_trace(E, args.requests * n)
     sampler = KernelSampler(dev0, every=4)
     budgets_seen = {}
@@ -274,7 +299,8 @@ def run_ours(args, d: Dist):
         tr = E.scale_to_rate(trace or base, rate_total)
         cl = GpuCluster(spec, shape, hw, slo, devices=devs, clock=clock, seed=args.seed,
                         resident_inputs=resident, weights=weights, budgets=args.budgets,
-                        pool_bytes_limit=pool_limit)
+                        pool_bytes_limit=pool_limit,
+                        emulated_link_gbs=args.emulate_link_gbs if emulated else None)
         budgets_seen.update({t.name: [b.token_budget, b.image_budget]
                              for t, b in cl.type_budgets.items()})
         if sample:
@@ -371,13 +397,18 @@ def run_ours(args, d: Dist):
                     "peak_source": f"{peak_src} hbm_gbs"}
         ach = s["work_per_ms"] / 1e9  # flop/ms -> TFLOP/s
         pk = peaks["bf16_tflops_sustained"]
+        busy = s["work_per_union_ms"] / 1e9
         return {"kernel": {"gemm": "gemm_tc_kernel + gemm_pair_kernel (K1, tcgen05)",
                            "prefill_attn": "attn_tc_kernel<128,paged> (K7, tcgen05)",
                            "vit_attn": "attn_tc_kernel<64,varlen> (K3, tcgen05)"}[name],
                 "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
                 "frac": ach / pk, "traffic": traffic_of(name), "launches_timed": s["launches"],
                 "avg_launch_ms": s["avg_ms"], "share_of_step": s["share_of_batch_time"],
-                "peak_source": f"{peak_src} bf16_tflops_sustained"}
+                "peak_source": f"{peak_src} bf16_tflops_sustained",
+                # the same flops over the time any launch of the class was running (the V and
+                # L streams overlap their kernels; per-launch durations count that time twice)
+                "achieved_over_busy_time": busy, "frac_over_busy_time": busy / pk,
+                "solo_achieved": s["solo_work_per_ms"] / 1e9, "solo_launches": s["solo_launches"]}
 
     roofline = roof(dominant) if dominant else None
     if roofline is not None and dominant == "gemm":
@@ -450,6 +481,10 @@ def run_ours(args, d: Dist):
         "config": cfg,
         "arm": {"executor": "libhydra_sm100.so (sm_100a) under the reference scheduler",
                 "devices": idx,
+                "emulated_gpus": (f"{n} GPU slots co-located on {len(phys)} device(s): each "
+                                  "batch is timed alone on the device (one batch in flight in "
+                                  "the replay), migrations charged max(measured copy, bytes / "
+                                  f"{args.emulate_link_gbs:g} GB/s)") if emulated else None,
                 "clock": "virtual clock advanced by the CUDA-event time of each batch",
                 "budgets": {"mode": args.budgets, "tau_t_tau_e": budgets_seen}},
         "decode_tok_s": best_probe["decode_tok_s"] if best_probe else 0.0,
@@ -741,7 +776,9 @@ def run_reference(args, d: Dist):
 
 
 def main():
+    global TRACE
     args = parse()
+    TRACE = args.trace
     d = Dist()
     try:
         if args.impl == "reference":

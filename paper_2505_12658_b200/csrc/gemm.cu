@@ -759,6 +759,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
     }
     fence_mbar_init();
   }
+  // both CTAs of the pair reach the collective allocation together (a cta_group::2 alloc
+  // before the peer has started was the one compute-sanitizer racecheck hazard)
+  cluster_sync();
   if (warp == 1) tmem_alloc_cg2(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   cluster_sync();

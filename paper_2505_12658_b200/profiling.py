@@ -54,6 +54,10 @@ class KernelSampler:
         # GPU to itself, so these durations are not inflated by the other stream's CTAs
         self.solo_samples: Dict[str, List] = {k: [] for k in self.CLASSES}
         self.solo = False
+        # busy time of the class: the union of its launches' [begin, end) intervals per
+        # sampled batch.  With the V and L streams running kernels of the same class at
+        # once, per-launch durations double-count the overlapped time; the union does not
+        self.union_ms: Dict[str, float] = {k: 0.0 for k in self.CLASSES}
         self.batch_ms: Dict[str, float] = {k: 0.0 for k in self.CLASSES}
         self.class_ms: Dict[str, float] = {k: 0.0 for k in self.CLASSES}
         self.order = list(self.CLASSES)
@@ -80,8 +84,11 @@ class KernelSampler:
         self.lib.hy_set_kernel_timer(None)
         name = self.active
         tot = 0.0
+        ivs = []
         for i in range(self.timer.count):
             ms = self.events[2 * i].elapsed_time(self.events[2 * i + 1])
+            t0 = self.events[0].elapsed_time(self.events[2 * i]) if i else 0.0
+            ivs.append((t0, t0 + ms))
             work = self._work[i]
             if name == "decode_attn":
                 work = decode_ctx_bytes
@@ -101,6 +108,18 @@ class KernelSampler:
                 acc[0] += ms
                 acc[1] += work
                 acc[2] += 1
+        ivs.sort()
+        busy, cur0, cur1 = 0.0, None, None
+        for x0, x1 in ivs:
+            if cur1 is None or x0 > cur1:
+                if cur1 is not None:
+                    busy += cur1 - cur0
+                cur0, cur1 = x0, x1
+            else:
+                cur1 = max(cur1, x1)
+        if cur1 is not None:
+            busy += cur1 - cur0
+        self.union_ms[name] += busy
         self.batch_ms[name] += batch_device_ms
         self.class_ms[name] += tot
         self.active = None
@@ -124,6 +143,9 @@ class KernelSampler:
             so_ms = sum(x for x, _ in so)
             out[name] = {"launches": len(s), "avg_ms": ms / len(s), "total_ms": ms,
                          "work": work, "work_per_ms": work / ms if ms > 0 else 0.0,
+                         "union_ms": self.union_ms[name],
+                         "work_per_union_ms": (work / self.union_ms[name]
+                                               if self.union_ms[name] > 0 else 0.0),
                          "solo_launches": len(so),
                          "solo_work_per_ms": sum(w for _, w in so) / so_ms if so_ms > 0 else 0.0,
                          "share_of_batch_time": (self.class_ms[name] / self.batch_ms[name]

@@ -35,6 +35,7 @@ def _worker(rank, world, port, out):
     from paper_2505_12658_b200.cluster import copy_bytes, instance_devices, plan_transfer
     d = bench.Dist()
     args = types.SimpleNamespace(gpus=1, method=None, model="llava-1.5-7b", requests=20,
+                                 trace="textcaps",
                                  rate_lo=16.0, rate_hi=128.0)
     n = bench.n_gpus(args, d)
     cfg = bench.workload_config(args, n)
