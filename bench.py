@@ -278,6 +278,14 @@ def run_ours(args, d: Dist):
     peaks, peak_src = measured_peaks()
     shape = P.get_shape(args.model)
     hw = P.b200_hardware()
+    # co-located instances (repeated --devices entries) split the device's memory; the
+    # reference's pool accounting (pool_capacities, cluster.py:127-144) is then given the
+    # same per-instance share, so every block it admits exists physically
+    share = max(idx.count(i) for i in phys)
+    pool_limit = None if share == 1 else int(130e9 / share / 1.1)
+    emulated = share > 1 and n > 1  # several GPU slots on one device (see GpuCluster)
+    if share > 1:
+        hw = P.b200_hardware(gpu_memory_bytes=hw.model_weight_bytes + pool_limit)
     method = cfg["method"]
     spec = C.ClusterSpec(method=C.DisaggregationMethod.parse(method))
     n_inst = sum(c for _, c in spec.method.counts)
@@ -286,10 +294,6 @@ def run_ours(args, d: Dist):
     lib = _lib.load()
     weights = {torch.device("cuda", i): DeviceWeights(shape, torch.device("cuda", i), args.seed)
                for i in phys}
-    # co-located instances (repeated --devices entries) split the device's pool memory
-    share = max(idx.count(i) for i in phys)
-    pool_limit = None if share == 1 else int(120e9 / share)
-    emulated = share > 1 and n > 1  # several GPU slots on one device (see GpuCluster)
     base, slo = base_trace(E, args.requests * n)
     sampler = KernelSampler(dev0, every=4)
     budgets_seen = {}
@@ -484,7 +488,10 @@ def run_ours(args, d: Dist):
                 "emulated_gpus": (f"{n} GPU slots co-located on {len(phys)} device(s): each "
                                   "batch is timed alone on the device (one batch in flight in "
                                   "the replay), migrations charged max(measured copy, bytes / "
-                                  f"{args.emulate_link_gbs:g} GB/s)") if emulated else None,
+                                  f"{args.emulate_link_gbs:g} GB/s); each slot has "
+                                  f"{hw.gpu_memory_bytes / 1e9:.0f} GB (weights + its pool "
+                                  "share) in the reference's pool accounting")
+                if emulated else None,
                 "clock": "virtual clock advanced by the CUDA-event time of each batch",
                 "budgets": {"mode": args.budgets, "tau_t_tau_e": budgets_seen}},
         "decode_tok_s": best_probe["decode_tok_s"] if best_probe else 0.0,

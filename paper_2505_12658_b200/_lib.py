@@ -13,6 +13,9 @@ from ctypes import (POINTER, Structure, c_char_p, c_float, c_int, c_int64, c_lon
                     c_size_t, c_uint64, c_ulonglong, c_void_p)
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libhydra_sm100.so")
+# lab variants (tools/lab: the same sources built with other compile-time budgets) are loaded
+# through HY_LIB_PATH; they are still this library, never a fallback
+LIB_PATH = os.environ.get("HY_LIB_PATH", LIB_PATH)
 
 HY_ACT_NONE = 0
 HY_ACT_QUICK_GELU = 1

@@ -34,6 +34,15 @@
 
 #include <algorithm>
 
+// operand-ring budgets (KB of shared memory per CTA); lab builds lower them to leave room
+// for co-resident CTAs of other kernels (tools/lab/build.sh overlap variants)
+#ifndef HY_GEMM_SMEM_KB
+#define HY_GEMM_SMEM_KB 196
+#endif
+#ifndef HY_PAIR_SMEM_KB
+#define HY_PAIR_SMEM_KB 200
+#endif
+
 namespace hy {
 
 #ifdef HY_TRACE
@@ -267,7 +276,7 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = (HY_GEMM_SMEM_KB * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int SMEM_BYTES =
@@ -713,7 +722,7 @@ struct GemmPairCfg {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = (HY_PAIR_SMEM_KB * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM_BYTES =

@@ -39,6 +39,14 @@ static int split_reserve_sms() {
   const char* e = getenv("HY_SPLIT_SMS");
   return e ? atoi(e) : 24;
 }
+// Decode / prefill split (HY_LANG_SPLIT_PD=<n>: batches with >= n decode rows and prefill
+// rows): the decode rows and the prefill rows run their whole layer stacks as two independent
+// row groups on two streams -- they share only the weights -- so one group's HBM-bound
+// decode attention can run while the other group's tensor-bound GEMMs do.
+static int split_pd_min_decodes() {
+  const char* e = getenv("HY_LANG_SPLIT_PD");
+  return e ? atoi(e) : 0;
+}
 
 struct Carve {
   uint8_t* base;
@@ -184,7 +192,21 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
   };
 
   const int split_min = split_min_decodes();
-  if (split_min > 0 && nd >= split_min) {
+  const int split_pd = split_pd_min_decodes();
+  if (split_pd > 0 && nd >= split_pd && np_rows > 0) {
+    cudaStream_t side = nullptr;
+    cudaEvent_t join = nullptr;
+    HY_RET_IF(side_fork(st, &side, &join));
+    int rc = 0;
+    for (int li = 0; li < m->n_layers && rc == 0; ++li) {
+      rc = layer(li, 0, 0, nd, nd, side, w.gemm_ws2, w.dec_ws);      // decode rows
+      if (rc == 0) rc = layer(li, 1, 0, nd, nd, side, w.gemm_ws2, w.dec_ws);
+      if (rc == 0) rc = layer(li, 0, nd, R, 0, st, w.gemm_ws, w.dec_ws2);  // prefill rows
+      if (rc == 0) rc = layer(li, 1, nd, R, 0, st, w.gemm_ws, w.dec_ws2);
+    }
+    HY_RET_IF(rc);
+    HY_RET_IF(side_join(st, side, join));
+  } else if (split_min > 0 && nd >= split_min) {
     // Two row groups on two streams (first half of the decode rows | the rest + prefill):
     // while one group's decode attention streams KV from HBM, the other group's GEMMs keep
     // the tensor cores busy.  GEMM grids leave split_reserve_sms() SMs to the attention.

@@ -224,3 +224,15 @@ def test_split_row_groups_parity(monkeypatch):
     res = oracle_replay(cl, shape, seed=0)
     assert res["max_abs_err"] <= LOGIT_ATOL, res
     assert res["tokens_equal"] + res["near_ties"] == res["rows"], res
+
+
+def test_split_decode_prefill_groups_parity(monkeypatch):
+    """HY_LANG_SPLIT_PD: decode rows and prefill rows run as two independent row groups on
+    two streams -- same scheduler decisions and logits as the one-stream path."""
+    monkeypatch.setenv("HY_LANG_SPLIT_PD", "1")
+    shape = get_shape("tiny")
+    g, cl, _ = _run("config1_2000rps", shape)
+    assert batch_log_digest(cl.batch_log) == g["sha"]
+    res = oracle_replay(cl, shape, seed=0)
+    assert res["max_abs_err"] <= LOGIT_ATOL, res
+    assert res["tokens_equal"] + res["near_ties"] == res["rows"], res

@@ -12,7 +12,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--variants", default="HY_LANG_SPLIT=16")
+    ap.add_argument("--lib", default=None, help="lab build of the library (HY_LIB_PATH)")
+    ap.add_argument("--mixes", default="64x700x512,128x700x1024,256x700x2048,128x300x2816",
+                    help="decodes x context x prefill-chunk list")
     args = ap.parse_args()
+    if args.lib:
+        os.environ["HY_LIB_PATH"] = args.lib
     import paper_2505_12658_b200 as P
     from paper_2505_12658_b200._epdsim import C, E, EN, MC
     from paper_2505_12658_b200.budgets import _Prober
@@ -26,7 +31,8 @@ def main():
     pool = rt.kv_pool
     variants = [{}] + [dict(kv.split("=") for kv in v.split(","))
                        for v in filter(None, args.variants.split(";"))]
-    for nd, ctx, npf in ((64, 700, 512), (128, 700, 1024), (256, 700, 2048), (128, 300, 2816)):
+    mixes = [tuple(int(v) for v in m.split("x")) for m in args.mixes.split(",")]
+    for nd, ctx, npf in mixes:
         reqs, entries = {}, []
         nblk = MC.kv_blocks_needed(ctx + 1)
         for i in range(nd):
