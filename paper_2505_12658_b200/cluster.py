@@ -217,8 +217,9 @@ class GpuCluster(C.Cluster):
         msg = MigrationMessage(
             job.kind, job.rid, iids.index(job.source), iids.index(job.target), r.kv_len,
             -1, int(job.kv_bytes + job.image_bytes), self.seed,
-            tuple(BlockMap(w, bb, tuple(a), tuple(b_)) for w, a, b_, _, _, bb, _, _ in maps
-                  if w != "last_tok"))
+            tuple(BlockMap(w, bb, tuple(a), tuple(b_), gb, tb)
+                  for w, a, b_, _, _, bb, gb, tb in maps if w != "last_tok"),
+            tuple(int(t) for t in src.prompt(r)) if job.kind == "ep" else ())
         self.transfer_stats["control_bytes"] = (self.transfer_stats.get("control_bytes", 0) +
                                                 len(msg.to_bytes()))
         self.last_migration_message = msg

@@ -10,11 +10,15 @@ descriptor of the request (the synthetic-input seed; a production trace would ca
 ids and image handles here).  The byte format is fixed little-endian and versioned, so it
 can cross processes (CUDA-IPC pools on separate ranks) or hosts unchanged:
 
-    header   magic b"HYMG", u16 version, u8 kind (0 = EP images, 1 = PD KV),
+    header   magic b"HYMG", u16 version (2), u8 kind (0 = EP images, 1 = PD KV),
              u8 n_maps, u32 source instance index, u32 target instance index,
-             i64 kv_len, i32 last_token, u64 payload bytes, u64 seed, u16 len(rid), rid utf-8
-    per map  u8 pool (0 = KV, 1 = image), u32 n, u64 block_bytes, n x i32 source ids,
-             n x i32 target ids
+             i64 kv_len, i32 last_token, u64 payload bytes, u64 seed, u16 len(rid), rid utf-8,
+             u32 n_prompt, n_prompt x i32 prompt token ids (the request's text content; an
+             EP target prefills with them)
+    per map  u8 pool (0 = KV, 1 = image), u32 n, u64 block_bytes, u64 group_bytes,
+             u64 tail_bytes, n x i32 source ids, n x i32 target ids -- the last block moves
+             only the first tail_bytes of each group_bytes group (token-exact,
+             hy_copy_blocks_tail), so sum over maps = payload bytes
 """
 
 from __future__ import annotations
@@ -24,11 +28,11 @@ from dataclasses import dataclass, field
 from typing import List, Tuple
 
 MAGIC = b"HYMG"
-VERSION = 1
+VERSION = 2
 KINDS = {"ep": 0, "pd": 1}
 POOLS = {"kv": 0, "image": 1}
 _HDR = struct.Struct("<4sHBBIIqiQQH")
-_MAP = struct.Struct("<BIQ")
+_MAP = struct.Struct("<BIQQQ")
 
 
 @dataclass(frozen=True)
@@ -37,12 +41,26 @@ class BlockMap:
     block_bytes: int
     src_ids: Tuple[int, ...]  # source page table (physical block ids, in sequence order)
     dst_ids: Tuple[int, ...]  # target page table
+    group_bytes: int = 0      # 0: whole blocks (group = block)
+    tail_bytes: int = 0       # valid bytes per group of the last block (0: whole group)
 
     def __post_init__(self):
         if self.pool not in POOLS:
             raise ValueError(f"pool must be one of {sorted(POOLS)}")
         if len(self.src_ids) != len(self.dst_ids):
             raise ValueError("source and target page tables differ in length")
+        g = self.group_bytes or self.block_bytes
+        if g <= 0 or self.block_bytes % g or not 0 <= self.tail_bytes <= g:
+            raise ValueError("group_bytes must divide block_bytes; 0 <= tail_bytes <= group")
+
+    @property
+    def bytes(self) -> int:
+        """Bytes this map moves (the last block token-exact)."""
+        n = len(self.src_ids)
+        if n == 0:
+            return 0
+        g = self.group_bytes or self.block_bytes
+        return (n - 1) * self.block_bytes + (self.block_bytes // g) * (self.tail_bytes or g)
 
 
 @dataclass(frozen=True)
@@ -56,6 +74,7 @@ class MigrationMessage:
     payload_bytes: int        # job.kv_bytes + job.image_bytes (cluster.py:411-413)
     seed: int = 0
     maps: Tuple[BlockMap, ...] = field(default_factory=tuple)
+    prompt_ids: Tuple[int, ...] = ()
 
     def to_bytes(self) -> bytes:
         if self.kind not in KINDS:
@@ -64,9 +83,11 @@ class MigrationMessage:
         out = [_HDR.pack(MAGIC, VERSION, KINDS[self.kind], len(self.maps), self.source,
                          self.target, self.kv_len, self.last_token, self.payload_bytes,
                          self.seed, len(rid)), rid]
+        npr = len(self.prompt_ids)
+        out.append(struct.pack(f"<I{npr}i", npr, *self.prompt_ids))
         for m in self.maps:
             n = len(m.src_ids)
-            out.append(_MAP.pack(POOLS[m.pool], n, m.block_bytes))
+            out.append(_MAP.pack(POOLS[m.pool], n, m.block_bytes, m.group_bytes, m.tail_bytes))
             out.append(struct.pack(f"<{n}i{n}i", *m.src_ids, *m.dst_ids))
         return b"".join(out)
 
@@ -81,16 +102,20 @@ class MigrationMessage:
         off = _HDR.size
         rid = buf[off:off + rid_len].decode()
         off += rid_len
+        (npr,) = struct.unpack_from("<I", buf, off)
+        off += 4
+        prompt = struct.unpack_from(f"<{npr}i", buf, off)
+        off += 4 * npr
         maps: List[BlockMap] = []
         inv_pool = {v: k for k, v in POOLS.items()}
         for _ in range(n_maps):
-            pool, n, bb = _MAP.unpack_from(buf, off)
+            pool, n, bb, gb, tb = _MAP.unpack_from(buf, off)
             off += _MAP.size
             ids = struct.unpack_from(f"<{n}i{n}i", buf, off)
             off += 8 * n
-            maps.append(BlockMap(inv_pool[pool], bb, tuple(ids[:n]), tuple(ids[n:])))
+            maps.append(BlockMap(inv_pool[pool], bb, tuple(ids[:n]), tuple(ids[n:]), gb, tb))
         if off != len(buf):
             raise ValueError("trailing bytes after the last block map")
         inv_kind = {v: k for k, v in KINDS.items()}
         return MigrationMessage(inv_kind[kind], rid, source, target, kv_len, last_token,
-                                payload, seed, tuple(maps))
+                                payload, seed, tuple(maps), tuple(prompt))

@@ -26,8 +26,8 @@ def test_round_trip(n_kv, n_img):
     m = _msg(n_kv, n_img)
     b = m.to_bytes()
     assert MigrationMessage.from_bytes(b) == m
-    # header + rid + per map header + 8 bytes per block
-    assert len(b) == 46 + len(m.rid) + sum(13 + 8 * len(x.src_ids) for x in m.maps)
+    # header + rid + prompt ids + per map header + 8 bytes per block
+    assert len(b) == 46 + len(m.rid) + 4 + sum(29 + 8 * len(x.src_ids) for x in m.maps)
 
 
 def test_rejects_bad_input():
