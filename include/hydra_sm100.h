@@ -133,13 +133,20 @@ int hy_rope_kv_append(void* qkv, int ld_qkv, int rows, int n_heads, int n_kv_hea
 
 /* ---------------- K8: paged-KV decode attention ---------------- */
 /* q: [n, ld_q] (q heads x d at column 0); ctx[i] keys of slot slots[i]; out [n, ld_o].
- * workspace: split-KV partials (hy_attn_decode_workspace_bytes). */
+ * workspace (hy_attn_decode_workspace_bytes): 256 B of ticket counters, then the split-KV
+ * partials; it must be ZERO before its first use and every call leaves the counters zero
+ * again (like the GEMM workspace).  Calls on different streams need different workspaces. */
 int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads, int n_kv_heads,
                          int head_dim, const int* slots, const int* ctx, int max_ctx,
                          const int* block_table, int bt_stride, const void* kv_layer,
                          long long block_stride, float scale, void* out, int ld_o,
                          void* workspace, size_t workspace_bytes, cudaStream_t stream);
 size_t hy_attn_decode_workspace_bytes(int n, int n_heads, int head_dim, int max_ctx);
+/* Kernel choice for MHA decode attention on the CALLING host thread: nw > 0 selects the
+ * bulk-copy kernel (K8b) with nw warps x spw ring stages per CTA -- built to share SMs with a
+ * GEMM on another stream; nw = 0 restores the default (register-load kernel K8).
+ * Supported (nw, spw): (1,4) (2,2) (2,3) (2,4) (4,1) (4,2).  Returns 0 or cudaErrorInvalidValue. */
+int hy_set_decode_kernel(int nw, int spw);
 
 /* ---------------- K7: paged prefill attention (causal with offset) ---------------- */
 /* sequence s owns query rows [qstart[s], qstart[s+1]) at positions offset[s] + i and

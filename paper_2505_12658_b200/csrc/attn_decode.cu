@@ -23,7 +23,10 @@ namespace hy {
 
 constexpr int DEC_WARPS = 4;
 
-template <int G>
+// CO = 1: the same kernel as a separate function whose shared-memory carveout is set to the
+// maximum, so its CTAs can share SMs with a GEMM (co-resident mode); CO = 0 keeps the
+// default carveout (a larger L1: ~13% faster when it runs alone, 7.0 vs 6.1 TB/s).
+template <int G, int CO = 0>
 __global__ void __launch_bounds__(128)
     attn_decode_kernel(const bf16* __restrict__ q, int ld_q, int n_kv, const int* __restrict__ slots,
                        const int* __restrict__ ctx_len, const int* __restrict__ block_table,
@@ -492,6 +495,223 @@ __global__ void attn_decode_combine_kernel(const float* __restrict__ part, int n
   out[(size_t)b * ld_o + (size_t)h * D + d] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
 }
 
+// K8b: MHA decode attention with the KV stream landing in shared memory through bulk
+// copies (cp.async.bulk + mbarrier) instead of register loads.
+//
+// Built to run on the SAME SMs as a tensor-bound GEMM of another row group (decode /
+// prefill split): a register-load kernel is capped by the L1 space its in-flight lines
+// need (28 KB beside a GEMM that takes the maximum shared carveout), while bulk copies land
+// in a small explicit ring -- NW warps x SPW stages x 8 KB (K and V tile of one 16-token
+// block of one head) -- that fits next to the GEMM's operand ring.  Each warp is an
+// independent pipeline: lane 0 issues the copies of the next stages (the item's q rides in
+// its first stage), all 32 lanes consume, and items (sequence, head, KV split) come from a
+// global ticket counter, so SMs slowed by a co-resident GEMM simply take fewer items.  The
+// last warp to finish resets the counter for the next launch.
+constexpr int DB_STAGE = 2 * HY_KV_BLOCK_TOKENS * 128 * 2 + 256;  // K | V | q (256 B)
+
+template <int NW, int SPW>
+__global__ void __launch_bounds__(32 * NW)
+    attn_decode_bulk_kernel(const bf16* __restrict__ q, int ld_q, int n, int n_heads,
+                            const int* __restrict__ slots, const int* __restrict__ ctx_len,
+                            const int* __restrict__ block_table, int bt_stride,
+                            const bf16* __restrict__ kv, long long block_stride, float scale_log2,
+                            int bps, int nsplit, bf16* __restrict__ out, int ld_o,
+                            float* __restrict__ part, int* __restrict__ ctr) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int D = 128;
+  extern __shared__ __align__(128) uint8_t db_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, dl = lane & 15;
+  uint8_t* ring = db_smem + (size_t)warp * SPW * DB_STAGE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(db_smem + (size_t)NW * SPW * DB_STAGE) + warp * SPW;
+  int2* meta = reinterpret_cast<int2*>(db_smem + (size_t)NW * SPW * DB_STAGE + NW * SPW * 8) +
+               warp * SPW;
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < SPW; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const int n_items = n * n_heads * nsplit;
+  const size_t head_bytes = (size_t)HY_KV_BLOCK_TOKENS * D;  // ELEMENTS of one head's tile
+  const size_t v_off = (size_t)n_heads * head_bytes;
+
+  // ---- load cursor (warp-uniform): current item, its block range, block ids in lanes
+  int l_item = -1, l_b = 0, l_h = 0, l_blk = 0, l_end = 0, l_first = 0, l_bid = 0;
+  int next_t = 0;
+  if (lane == 0) next_t = atomicAdd(ctr, 1);
+  next_t = __shfl_sync(0xffffffffu, next_t, 0);
+  bool exhausted = false;
+  auto advance_item = [&]() {
+    while (true) {
+      const int t = next_t;
+      if (t >= n_items) {
+        exhausted = true;
+        return;
+      }
+      int nt = 0;
+      if (lane == 0) nt = atomicAdd(ctr, 1);  // one ticket ahead: latency overlaps this item
+      next_t = __shfl_sync(0xffffffffu, nt, 0);
+      const int sp = t / (n * n_heads);
+      const int r = t - sp * n * n_heads;
+      const int b = r / n_heads, h = r - b * n_heads;
+      const int nblk = (ctx_len[b] + HY_KV_BLOCK_TOKENS - 1) / HY_KV_BLOCK_TOKENS;
+      const int b0 = sp * bps, b1 = min(nblk, b0 + bps);
+      if (b0 >= b1) continue;  // empty split of a short sequence
+      l_item = t;
+      l_b = b;
+      l_h = h;
+      l_blk = l_first = b0;
+      l_end = b1;
+      const int* bt = block_table + (size_t)slots[b] * bt_stride;
+      l_bid = b0 + lane < b1 ? bt[b0 + lane] : 0;  // bps <= 32
+      return;
+    }
+  };
+  auto issue = [&](int st) {
+    if (!exhausted && l_blk >= l_end) advance_item();
+    const uint32_t sb = smem_u32(ring + (size_t)st * DB_STAGE);
+    if (exhausted) {
+      if (lane == 0) {
+        meta[st] = make_int2(-1, 0);
+        mbar_arrive(&bar[st]);
+      }
+      return;
+    }
+    const int bid = __shfl_sync(0xffffffffu, l_bid, l_blk - l_first);
+    if (lane == 0) {
+      const bool first = l_blk == l_first;
+      meta[st] = make_int2(l_item, l_blk | (first ? (1 << 30) : 0));
+      fence_proxy_async_smem();  // the consumer's reads of this stage precede the refill
+      mbar_expect_tx(&bar[st], 2 * head_bytes * 2 + (first ? D * 2 : 0));
+      const bf16* kb = kv + (size_t)bid * block_stride + (size_t)l_h * head_bytes;
+      bulk_load_1d(sb, kb, head_bytes * 2, smem_u32(&bar[st]), kEvictFirst);
+      bulk_load_1d(sb + head_bytes * 2, kb + v_off, head_bytes * 2, smem_u32(&bar[st]), kEvictFirst);
+      if (first)
+        bulk_load_1d(sb + 4 * head_bytes, q + (size_t)l_b * ld_q + (size_t)l_h * D, D * 2,
+                     smem_u32(&bar[st]), kEvictFirst);
+    }
+    ++l_blk;
+  };
+
+#pragma unroll
+  for (int st = 0; st < SPW; ++st) issue(st);
+
+  // ---- consumer
+  int c_item = -1, c_ctx = 0;
+  float qf[8], m = -INFINITY, l = 0.f, acc[8];
+  auto finish = [&]() {
+    if (c_item < 0) return;
+    l += __shfl_xor_sync(0xffffffffu, l, 16);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
+    const int sp = c_item / (n * n_heads);
+    const int r = c_item - sp * n * n_heads;  // = b * n_heads + h
+    if (half == 0) {
+      if (nsplit == 1) {
+        const int b = r / n_heads, h = r - b * n_heads;
+        float o[8];
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = acc[j] * inv;
+        store_bf16x8(out + (size_t)b * ld_o + (size_t)h * D + dl * 8, o);
+      } else {
+        float* pp = part + ((size_t)r * nsplit + sp) * (D + 2);
+        float2* p2 = reinterpret_cast<float2*>(pp + dl * 8);  // rows of D + 2 floats: 8B aligned
+#pragma unroll
+        for (int j = 0; j < 4; ++j) p2[j] = make_float2(acc[2 * j], acc[2 * j + 1]);
+        if (dl == 0) {
+          pp[D] = m;
+          pp[D + 1] = l;
+        }
+      }
+    }
+  };
+  int st = 0;
+  uint32_t ph = 0;
+  while (true) {
+    mbar_wait(&bar[st], ph);
+    const int2 md = meta[st];
+    if (md.x < 0) break;
+    const uint32_t sb = smem_u32(ring + (size_t)st * DB_STAGE);
+    if (md.x != c_item) {
+      finish();
+      c_item = md.x;
+      c_ctx = ctx_len[(md.x % (n * n_heads)) / n_heads];
+      m = -INFINITY;
+      l = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+      const float4 q0 = lds_f32x4(sb + 4 * head_bytes + dl * 16);
+      const uint32_t qw[4] = {__float_as_uint(q0.x), __float_as_uint(q0.y), __float_as_uint(q0.z),
+                              __float_as_uint(q0.w)};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = unpack_bf16x2(qw[j]);
+        qf[2 * j] = f.x * scale_log2;
+        qf[2 * j + 1] = f.y * scale_log2;
+      }
+    }
+    const int jb = md.y & ((1 << 30) - 1);
+    const int ctx = c_ctx;
+    const int tok_base = jb * HY_KV_BLOCK_TOKENS + half;
+    float s[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 kq = lds_f32x4(sb + (2 * i + half) * D * 2 + dl * 16);
+      const float2 k0 = unpack_bf16x2(__float_as_uint(kq.x)), k1 = unpack_bf16x2(__float_as_uint(kq.y)),
+                   k2 = unpack_bf16x2(__float_as_uint(kq.z)), k3 = unpack_bf16x2(__float_as_uint(kq.w));
+      float d0 = qf[0] * k0.x + qf[1] * k0.y + qf[2] * k1.x + qf[3] * k1.y + qf[4] * k2.x +
+                 qf[5] * k2.y + qf[6] * k3.x + qf[7] * k3.y;
+      d0 += __shfl_xor_sync(0xffffffffu, d0, 8);
+      d0 += __shfl_xor_sync(0xffffffffu, d0, 4);
+      d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
+      d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
+      s[i] = (tok_base + 2 * i < ctx) ? d0 : -INFINITY;
+    }
+    float mb = s[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) mb = fmaxf(mb, s[i]);
+    mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, 16));
+    const float mn = fmaxf(m, mb);  // finite: every block holds >= 1 valid token
+    const float corr = exp2f(m - mn);
+    m = mn;
+    float ls = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] *= corr;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float p = exp2f(s[i] - mn);
+      ls += p;
+      const float4 vq = lds_f32x4(sb + 2 * head_bytes + (2 * i + half) * D * 2 + dl * 16);
+      const float2 v0 = unpack_bf16x2(__float_as_uint(vq.x)), v1 = unpack_bf16x2(__float_as_uint(vq.y)),
+                   v2 = unpack_bf16x2(__float_as_uint(vq.z)), v3 = unpack_bf16x2(__float_as_uint(vq.w));
+      acc[0] += p * v0.x; acc[1] += p * v0.y;
+      acc[2] += p * v1.x; acc[3] += p * v1.y;
+      acc[4] += p * v2.x; acc[5] += p * v2.y;
+      acc[6] += p * v3.x; acc[7] += p * v3.y;
+    }
+    l = l * corr + ls;
+    __syncwarp();  // every lane has read the stage before lane 0 refills it
+    issue(st);
+    if (++st == SPW) {
+      st = 0;
+      ph ^= 1;
+    }
+  }
+  finish();
+  // the last warp of the grid resets the ticket counter (every warp has taken its last
+  // ticket before it counts itself done)
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1) == (int)(gridDim.x * NW) - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+}
+
 // KV splits per (sequence, KV head): enough CTAs for ~per_sm per SM.  GQA CTAs (G >= 4
 // query heads per KV head, tensor-core kernel) aim for 4 per SM -- each already does G
 // heads of work per byte, and fewer splits save the combine pass (Qwen2-VL 28/4, 256 x 660
@@ -514,9 +734,100 @@ static int decode_splits(int n, int n_kv, int max_ctx, int G = 1) {
 
 using namespace hy;
 
+// Workspace: [ticket counters: 256 B, zero between launches][split-KV partials]
+static constexpr size_t kDecCtrBytes = 256;
+
 extern "C" size_t hy_attn_decode_workspace_bytes(int n, int n_heads, int head_dim, int max_ctx) {
   const int ns = decode_splits(n, n_heads, max_ctx);  // n_kv <= n_heads: upper bound
-  return (size_t)n * n_heads * std::max(ns, 64) * (head_dim + 2) * sizeof(float);
+  return kDecCtrBytes + (size_t)n * n_heads * std::max(ns, 64) * (head_dim + 2) * sizeof(float);
+}
+
+namespace hy {
+// Per-thread choice of the MHA decode kernel (decode_set_coresident): the bulk-copy kernel
+// when the decode attention is meant to share SMs with another stream's GEMM.
+static thread_local int t_dec_coresident = 0;
+static thread_local int t_dec_nw = 0, t_dec_spw = 0;  // hy_set_decode_kernel
+void decode_set_coresident(int on) { t_dec_coresident = on; }
+
+struct BulkCfg {
+  int nw, spw;
+};
+// HY_DECODE_BULK=<nw>,<spw> forces the bulk kernel everywhere (A/B).  Measured beside a GEMM
+// it does not pay: one 34 KB CTA per SM keeps too few bytes in flight (2.5-3.5 TB/s alone,
+// tools/overlap_lab.py), so co-resident launches use K8 with the maximum carveout instead.
+static BulkCfg bulk_cfg() {
+  static const BulkCfg env = [] {
+    BulkCfg c{0, 0};
+    if (const char* e = getenv("HY_DECODE_BULK")) sscanf(e, "%d,%d", &c.nw, &c.spw);
+    return c;
+  }();
+  if (t_dec_nw > 0) return BulkCfg{t_dec_nw, t_dec_spw};
+  return env;
+}
+
+template <int NW, int SPW>
+static int launch_bulk(const bf16* q, int ld_q, int n, int n_heads, const int* slots,
+                       const int* ctx, int max_ctx, const int* bt, int bt_stride, const bf16* kv,
+                       long long block_stride, float sl2, bf16* out, int ld_o, uint8_t* ws,
+                       size_t ws_bytes, cudaStream_t stream) {
+  constexpr int SMEM = NW * SPW * (DB_STAGE + 8 + 8);
+  auto kern = attn_decode_bulk_kernel<NW, SPW>;
+  HY_CUDA_RET(ensure_smem(kern, SMEM));
+  HY_CUDA_RET(ensure_max_carveout(kern));
+  static thread_local int occ_dev = -1, occ = 0;
+  int dev = 0;
+  HY_CUDA_RET(cudaGetDevice(&dev));
+  if (occ_dev != dev) {
+    HY_CUDA_RET(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * NW, SMEM));
+    occ_dev = dev;
+  }
+  const int max_blocks = std::max(1, ceil_div(max_ctx, HY_KV_BLOCK_TOKENS));
+  // items: >= ~8 per warp of one CTA per SM, at most 32 blocks each (block ids in lanes)
+  const int want = 8 * num_sms() * NW;
+  int ns = std::max(1, std::min(ceil_div(want, std::max(1, n * n_heads)), ceil_div(max_blocks, 4)));
+  int bps = std::min(32, ceil_div(max_blocks, ns));
+  ns = ceil_div(max_blocks, bps);
+  const size_t need = kDecCtrBytes + (size_t)n * n_heads * ns * (128 + 2) * sizeof(float);
+  if (ns > 1 && need > ws_bytes) {
+    set_last_error("decode attention: workspace too small for the bulk kernel");
+    return (int)cudaErrorInvalidValue;
+  }
+  const long long items = (long long)n * n_heads * ns;
+  // CTAs per SM: the occupancy limit alone; ONE beside a GEMM (co-resident mode), so the
+  // persistent CTAs never take the shared memory a GEMM CTA needs on any SM
+  static const int env_cps = [] {
+    const char* e = getenv("HY_DECODE_BULK_CPS");
+    return e ? atoi(e) : 0;
+  }();
+  const int cps = env_cps > 0 ? env_cps : t_dec_coresident ? 1 : std::max(occ, 1);
+  const int grid = (int)std::max<long long>(
+      1, std::min<long long>((long long)num_sms() * std::min(cps, std::max(occ, 1)),
+                             ceil_div(items, NW)));
+  int* ctr = reinterpret_cast<int*>(ws);
+  float* part = reinterpret_cast<float*>(ws + kDecCtrBytes);
+  HY_CUDA_RET(launch_pdl(kern, dim3(grid), dim3(32 * NW), (size_t)SMEM, stream, q, ld_q, n,
+                         n_heads, slots, ctx, bt, bt_stride, kv, block_stride, sl2, bps, ns, out,
+                         ld_o, part, ctr));
+  HY_LAUNCH_CHECK();
+  if (ns > 1) {
+    HY_CUDA_RET(launch_pdl(attn_decode_combine_kernel, dim3(n, n_heads), dim3(128), 0, stream,
+                           (const float*)part, n_heads, ns, out, ld_o));
+    HY_LAUNCH_CHECK();
+  }
+  return 0;
+}
+}  // namespace hy
+
+extern "C" int hy_set_decode_kernel(int nw, int spw) {
+  const bool ok = nw == 0 || (nw == 1 && spw == 4) || (nw == 2 && spw >= 2 && spw <= 4) ||
+                  (nw == 4 && (spw == 1 || spw == 2));
+  if (!ok) {
+    set_last_error("hy_set_decode_kernel: unsupported warps / stages");
+    return (int)cudaErrorInvalidValue;
+  }
+  hy::t_dec_nw = nw;
+  hy::t_dec_spw = spw;
+  return 0;
 }
 
 extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads, int n_kv_heads,
@@ -528,6 +839,34 @@ extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads,
   HY_CHECK_ARG(n_kv_heads > 0 && n_heads % n_kv_heads == 0, "heads");
   if (n <= 0) return 0;
   const int G = n_heads / n_kv_heads;
+  if (G == 1) {
+    const BulkCfg bc = bulk_cfg();
+    if (bc.nw > 0) {
+      uint8_t* wsb = reinterpret_cast<uint8_t*>(workspace);
+      HY_CHECK_ARG(wsb != nullptr && workspace_bytes >= kDecCtrBytes, "decode workspace");
+      const bf16* qp = reinterpret_cast<const bf16*>(q);
+      const bf16* kvp = reinterpret_cast<const bf16*>(kv_layer);
+      bf16* op = reinterpret_cast<bf16*>(out);
+      const float sl2 = scale * 1.4426950408889634f;
+#define HY_BULK(NW, SPW)                                                                    \
+  if (bc.nw == NW && bc.spw == SPW)                                                         \
+    return launch_bulk<NW, SPW>(qp, ld_q, n, n_heads, slots, ctx, max_ctx, block_table,     \
+                                bt_stride, kvp, block_stride, sl2, op, ld_o, wsb,           \
+                                workspace_bytes, stream);
+      HY_BULK(1, 4)
+      HY_BULK(2, 2)
+      HY_BULK(2, 3)
+      HY_BULK(2, 4)
+      HY_BULK(4, 1)
+      HY_BULK(4, 2)
+#undef HY_BULK
+      set_last_error("decode attention: no bulk kernel for this warp / stage count");
+      return (int)cudaErrorInvalidValue;
+    }
+  }
+  // split-KV partials follow the ticket counters (the bulk kernel's layout)
+  workspace = workspace ? reinterpret_cast<uint8_t*>(workspace) + kDecCtrBytes : nullptr;
+  workspace_bytes = workspace_bytes > kDecCtrBytes ? workspace_bytes - kDecCtrBytes : 0;
   int ns = decode_splits(n, n_kv_heads, max_ctx, G);
   const size_t need = (size_t)n * n_heads * ns * (head_dim + 2) * sizeof(float);
   if (ns > 1 && (workspace == nullptr || need > workspace_bytes)) ns = 1;
@@ -540,11 +879,20 @@ extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads,
   const bf16* kvp = reinterpret_cast<const bf16*>(kv_layer);
   bf16* op = reinterpret_cast<bf16*>(out);
   float* part = reinterpret_cast<float*>(workspace);
+  static const bool carve_env = getenv("HY_DECODE_CARVEOUT") != nullptr;
+  const bool co = carve_env || t_dec_coresident;
 #define HY_DEC_CASE(GG)                                                                        \
   case GG:                                                                                     \
-    HY_CUDA_RET(launch_pdl(attn_decode_kernel<GG>, dim3(grid), dim3(128), 0, stream, qp, ld_q, n_kv_heads, slots, ctx,         \
-                                                     block_table, bt_stride, kvp, block_stride, \
-                                                     sl2, bps, op, ld_o, part, ns));            \
+    if (co) {                                                                                  \
+      HY_CUDA_RET(ensure_max_carveout(attn_decode_kernel<GG, 1>));                             \
+      HY_CUDA_RET(launch_pdl(attn_decode_kernel<GG, 1>, dim3(grid), dim3(128), 0, stream, qp,  \
+                             ld_q, n_kv_heads, slots, ctx, block_table, bt_stride, kvp,        \
+                             block_stride, sl2, bps, op, ld_o, part, ns));                     \
+    } else {                                                                                   \
+      HY_CUDA_RET(launch_pdl(attn_decode_kernel<GG>, dim3(grid), dim3(128), 0, stream, qp,     \
+                             ld_q, n_kv_heads, slots, ctx, block_table, bt_stride, kvp,        \
+                             block_stride, sl2, bps, op, ld_o, part, ns));                     \
+    }                                                                                          \
     break;
   if (G >= 4 && G <= 16 && !getenv("HY_DECODE_GQA_CUDA")) {
     HY_CUDA_RET(ensure_smem(attn_decode_gqa_mma_kernel,

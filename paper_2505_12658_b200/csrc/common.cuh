@@ -219,6 +219,16 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* tm, uint64_t* bar
       : "memory");
 }
 
+// 1D bulk copy global -> shared (no tensor map), completes its bytes on bar.
+__device__ __forceinline__ void bulk_load_1d(uint32_t dst, const void* src, uint32_t bytes,
+                                             uint32_t bar, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(cache_hint)
+      : "memory");
+}
+
 // Prefetch a 2D TMA box into L2 (no shared-memory destination, no completion tracking).
 // TMA store shared -> global (bulk-group completion) and its group waits
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, uint32_t src, int c0, int c1) {
@@ -458,6 +468,15 @@ cudaError_t ensure_smem_attr(const void* kernel, int bytes);
 template <typename... KArgs>
 inline cudaError_t ensure_smem(void (*kernel)(KArgs...), int bytes) {
   return ensure_smem_attr(reinterpret_cast<const void*>(kernel), bytes);
+}
+
+// Ask for the maximum shared-memory carveout for a kernel on the CURRENT device.  CTAs of
+// kernels with different L1 / shared splits cannot share an SM, so a small-smem kernel meant
+// to run beside the GEMM (whose carveout is the maximum) must request the same split.
+cudaError_t ensure_max_carveout_attr(const void* kernel);
+template <typename... KArgs>
+inline cudaError_t ensure_max_carveout(void (*kernel)(KArgs...)) {
+  return ensure_max_carveout_attr(reinterpret_cast<const void*>(kernel));
 }
 
 // kernel-class timer hooks (see hy_set_kernel_timer)

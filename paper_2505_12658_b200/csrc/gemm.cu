@@ -120,7 +120,7 @@ constexpr int kStgStride = 32 * 4 + 16;  // bytes per staged row (pad: conflict-
 constexpr int kStgBytes = 4096;
 static_assert(16 * kStgStride <= kStgBytes, "swap staging");
 
-template <int EPI, bool SWAP>
+template <int EPI, bool SWAP, bool STG_DBL = true>
 __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int p0, int q0, float* v, int lane,
                                           uint32_t stg, const CUtensorMap* tmC, int& nst) {
   constexpr int OC = EPI == EPI_SWIGLU ? 16 : 32;  // output columns of this chunk
@@ -153,8 +153,13 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& a, int p0, int q0, flo
       // TMA-store epilogue: the warp's 32 rows x OC bf16 go through one of two shared
       // buffers and leave as one bulk tensor store (full row segments, asynchronous), instead
       // of 32 scattered 16-byte pieces per store instruction.  Rows >= M are clipped by TMA.
-      const uint32_t buf = stg + (nst & 1) * (kStgBytes / 2);
-      if (lane == 0) bulk_wait_read<1>();  // this buffer's store (two chunks ago) has read it
+      const uint32_t buf = stg + (STG_DBL ? (nst & 1) * (kStgBytes / 2) : 0);
+      if (lane == 0) {  // this buffer's previous store (two chunks ago / the last one) has read it
+        if (STG_DBL)
+          bulk_wait_read<1>();
+        else
+          bulk_wait_read<0>();
+      }
       __syncwarp();
       if (m < a.M && a.residual) {
         const bf16* r = a.residual + (size_t)m * a.ldr + col0;
@@ -716,6 +721,14 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
 // release the accumulator on the leader's accumulator-empty barrier.  Each CTA's TMEM
 // holds its own 128 rows of the 256 x BN accumulator (double-buffered).
 // ---------------------------------------------------------------------------
+// The pair kernel's per-warp TMA-store staging: two 2 KB buffers (default), or one
+// (HY_PAIR_STG_BYTES=2048, co-resident lab builds: 16 KB less shared memory per CTA)
+#ifndef HY_PAIR_STG_BYTES
+#define HY_PAIR_STG_BYTES 4096
+#endif
+constexpr int kPairStgBytes = HY_PAIR_STG_BYTES;
+constexpr bool kPairStgDbl = kPairStgBytes >= 4096;
+
 template <int BN>
 struct GemmPairCfg {
   static constexpr int BK = 64;
@@ -726,7 +739,7 @@ struct GemmPairCfg {
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM_BYTES =
-      STAGES * STAGE_BYTES + kEpiWarps * kStgBytes + 1024 /*align*/ + 256 /*barriers*/;
+      STAGES * STAGE_BYTES + kEpiWarps * kPairStgBytes + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int THREADS = 64 + 32 * kEpiWarps;
 };
 
@@ -741,7 +754,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint8_t* stg_base = smem + C::STAGES * C::STAGE_BYTES;  // epilogue TMA-store buffers
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + kEpiWarps * kStgBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + kEpiWarps * kPairStgBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
@@ -939,8 +952,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
                          (((size_t)(cc * 2 + slot) * 2 + rank) * (BN / 32) + c) * 8 * 128 + lrow;
           }
           add_partials(v, srcs, ns, nb);
-          epi_chunk<EPI, false>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32, v, lane,
-                                smem_u32(stg_base) + (warp - 2) * kStgBytes, &tmC, nst);
+          epi_chunk<EPI, false, kPairStgDbl>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32,
+                                             v, lane, smem_u32(stg_base) + (warp - 2) * kPairStgBytes,
+                                             &tmC, nst);
         }
       }
       tc_fence_before();

@@ -195,7 +195,7 @@ def test_decode_attention(n_heads, n_kv, ctxs):
     slots = torch.arange(n, device=DEV, dtype=torch.int32)
     ctx = torch.tensor(ctxs, device=DEV, dtype=torch.int32)
     wsb = lib().hy_attn_decode_workspace_bytes(n, n_heads, d, max(ctxs))
-    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=DEV)
+    ws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=DEV)
     layer_ptr = kv.data_ptr() + layer * 2 * n_kv * 16 * d * 2
     ck(lib().hy_attn_decode_paged(q.data_ptr(), n_heads * d, n, n_heads, n_kv, d,
                                   slots.data_ptr(), ctx.data_ptr(), max(ctxs), bt.data_ptr(), bts,
@@ -210,6 +210,49 @@ def test_decode_attention(n_heads, n_kv, ctxs):
         s = torch.einsum("hd,thd->ht", qi, Kx) / math.sqrt(d)
         ref = torch.einsum("ht,thd->hd", torch.softmax(s, -1), Vx).reshape(-1)
         assert (out[i].float() - ref).abs().max().item() < 2e-2, (i, c)
+
+
+@pytest.mark.parametrize("cfg", [(2, 2), (4, 1), (1, 4), (2, 4)])
+@pytest.mark.parametrize("ctxs", [
+    [1, 17, 300, 33, 616, 617, 2000],
+    [16 * 64 * 3 + 5, 15, 16],                 # long context: many KV splits + combine
+    list(range(1, 400, 7)),                    # many items per warp, empty splits
+])
+def test_decode_attention_bulk(cfg, ctxs):
+    """K8b (bulk-copy decode kernel) vs the fp32 reference; called twice on the same
+    workspace, so the ticket counter must have been reset by the first call."""
+    n_heads = n_kv = 8
+    d, L, layer = 128, 2, 1
+    n = len(ctxs)
+    kv, bt, bts, be = _paged_setup(n, ctxs, n_kv, d, L, layer)
+    q = torch.randn(n, n_heads * d, device=DEV).bfloat16()
+    slots = torch.arange(n, device=DEV, dtype=torch.int32)
+    ctx = torch.tensor(ctxs, device=DEV, dtype=torch.int32)
+    wsb = lib().hy_attn_decode_workspace_bytes(n, n_heads, d, max(ctxs))
+    ws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=DEV)
+    layer_ptr = kv.data_ptr() + layer * 2 * n_kv * 16 * d * 2
+    outs = []
+    ck(lib().hy_set_decode_kernel(*cfg), "set kernel")
+    try:
+        for _ in range(2):
+            out = torch.empty(n, n_heads * d, device=DEV, dtype=torch.bfloat16)
+            ck(lib().hy_attn_decode_paged(q.data_ptr(), n_heads * d, n, n_heads, n_kv, d,
+                                          slots.data_ptr(), ctx.data_ptr(), max(ctxs),
+                                          bt.data_ptr(), bts, layer_ptr, be, 1 / math.sqrt(d),
+                                          out.data_ptr(), n_heads * d, ws.data_ptr(), ws.numel(),
+                                          st()), "decode bulk")
+            outs.append(out)
+    finally:
+        lib().hy_set_decode_kernel(0, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    assert ws[:8].view(torch.int32).tolist() == [0, 0]  # counters reset for the next launch
+    for i, c in enumerate(ctxs):
+        K, V = _gather_kv(kv, bt, i, c, L, layer, n_kv, d)
+        qi = q[i].float().view(n_heads, d)
+        s = torch.einsum("hd,thd->ht", qi, K) / math.sqrt(d)
+        ref = torch.einsum("ht,thd->hd", torch.softmax(s, -1), V).reshape(-1)
+        assert (outs[0][i].float() - ref).abs().max().item() < 2e-2, (i, c)
 
 
 @pytest.mark.parametrize("n_heads,n_kv,chunks", [

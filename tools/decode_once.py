@@ -19,7 +19,7 @@ q = torch.randn(n, nh * d, device="cuda").bfloat16()
 o = torch.empty_like(q)
 slots = torch.arange(n, dtype=torch.int32, device="cuda")
 ctxs = torch.full((n,), ctx, dtype=torch.int32, device="cuda")
-ws = torch.empty(max(lib.hy_attn_decode_workspace_bytes(n, nh, d, ctx), 16), dtype=torch.uint8,
+ws = torch.zeros(max(lib.hy_attn_decode_workspace_bytes(n, nh, d, ctx), 16), dtype=torch.uint8,
                  device="cuda")
 for _ in range(3):
     rc = lib.hy_attn_decode_paged(q.data_ptr(), nh * d, n, nh, nkv, d, slots.data_ptr(),

@@ -226,7 +226,7 @@ def overlap_probe(out):
     slots = torch.arange(n, dtype=torch.int32, device=DEV)
     ctxs = torch.full((n,), ctx, dtype=torch.int32, device=DEV)
     wsb = lib().hy_attn_decode_workspace_bytes(n, nh, d, ctx)
-    dws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=DEV)
+    dws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=DEV)
     M, N, K = 2304, 22016, 4096
     A = torch.randn(M, K, device=DEV).bfloat16()
     W = (torch.randn(N, K, device=DEV) * 0.02).bfloat16()
@@ -298,7 +298,7 @@ def decode_sweep(out):
         slots = torch.arange(n, dtype=torch.int32, device=DEV)
         ctxs = torch.full((n,), ctx, dtype=torch.int32, device=DEV)
         wsb = lib().hy_attn_decode_workspace_bytes(n, nh, d, ctx)
-        ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=DEV)
+        ws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=DEV)
 
         def ours(i):
             rc = lib().hy_attn_decode_paged(q.data_ptr(), nh * d, n, nh, nkv, d, slots.data_ptr(),

@@ -24,12 +24,15 @@ def main():
     ap.add_argument("--M", type=int, default=3000)
     ap.add_argument("--seqs", type=int, default=400)
     ap.add_argument("--ctx", type=int, default=700)
+    ap.add_argument("--bulk", default="0,0", help="decode kernel: nw,spw of the bulk kernel (0,0 = K8)")
     args = ap.parse_args()
     if args.lib:
         os.environ["HY_LIB_PATH"] = args.lib
     import torch
     from paper_2505_12658_b200 import _lib
     lib = _lib.load()
+    nw, spw = (int(x) for x in args.bulk.split(","))
+    assert lib.hy_set_decode_kernel(nw, spw) == 0, lib.hy_last_error()
     dev = "cuda:0"
     M, N, K = args.M, 12288, 4096
     A = torch.randn(M, K, device=dev).bfloat16()
@@ -48,7 +51,7 @@ def main():
     slots = torch.arange(n, dtype=torch.int32, device=dev)
     ctxs = torch.full((n,), ctx, dtype=torch.int32, device=dev)
     wsb = lib.hy_attn_decode_workspace_bytes(n, nh, d, ctx)
-    dws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)
+    dws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=dev)
     s1 = torch.cuda.Stream(dev)
     s2 = torch.cuda.Stream(dev)
 
@@ -89,7 +92,7 @@ def main():
     ta = timed(lambda: attn(cur))
     tb = timed(both)
     kv_bytes = n * ctx * 2 * nh * d * 2
-    print(f"lib {os.path.basename(_lib.LIB_PATH)}  M={M}: gemm {tg:.1f} us "
+    print(f"lib {os.path.basename(_lib.LIB_PATH)} bulk {args.bulk} M={M}: gemm {tg:.1f} us "
           f"({2 * M * N * K / tg / 1e6:.0f} TF/s) | decode attn {n}x{ctx} {ta:.1f} us "
           f"({kv_bytes / ta / 1e3:.0f} GB/s) | both {tb:.1f} us (sum {tg + ta:.1f}, "
           f"max {max(tg, ta):.1f}, overlap {(tg + ta - tb) / min(tg, ta):.0%})", flush=True)

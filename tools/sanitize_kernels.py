@@ -113,7 +113,7 @@ def decode(n_heads, n_kv, ctxs):
     slots = torch.arange(n, dtype=torch.int32, device=DEV)
     ctx = torch.tensor(ctxs, dtype=torch.int32, device=DEV)
     wsb = lib.hy_attn_decode_workspace_bytes(n, n_heads, d, max(ctxs))
-    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=DEV)
+    ws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=DEV)
     ck(lib.hy_attn_decode_paged(q.data_ptr(), n_heads * d, n, n_heads, n_kv, d,
                                 slots.data_ptr(), ctx.data_ptr(), max(ctxs), bt.data_ptr(), bts,
                                 kv.data_ptr() + 2 * n_kv * blk * d * 2, L * 2 * n_kv * blk * d,
