@@ -145,8 +145,13 @@ size_t hy_attn_decode_workspace_bytes(int n, int n_heads, int head_dim, int max_
 /* Kernel choice for MHA decode attention on the CALLING host thread: nw > 0 selects the
  * bulk-copy kernel (K8b) with nw warps x spw ring stages per CTA -- built to share SMs with a
  * GEMM on another stream; nw = 0 restores the default (register-load kernel K8).
- * Supported (nw, spw): (1,4) (2,2) (2,3) (2,4) (4,1) (4,2).  Returns 0 or cudaErrorInvalidValue. */
+ * Supported (nw, spw): (1,4) (1,5) (2,2) (2,3) (2,4) (4,1) (4,2) (4,6) (5,1) (8,3).  Returns 0 or cudaErrorInvalidValue. */
 int hy_set_decode_kernel(int nw, int spw);
+/* Co-resident mode for decode attention on the CALLING host thread (on != 0): the
+ * tensor-core kernel K8c that shares every SM with a running GEMM -- at most one CTA per SM,
+ * a ~36 KB shared-memory ring -- for GQA groups 1 and 7; other groups use the default kernel.
+ * hy_lang_forward's decode / prefill split turns it on for its decode rows. */
+int hy_set_decode_coresident(int on);
 
 /* ---------------- K7: paged prefill attention (causal with offset) ---------------- */
 /* sequence s owns query rows [qstart[s], qstart[s+1]) at positions offset[s] + i and

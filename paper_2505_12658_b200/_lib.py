@@ -128,6 +128,7 @@ _SIGS = {
                                      c_float, c_void_p, c_int, c_void_p, c_size_t, c_void_p]),
     "hy_attn_decode_workspace_bytes": (c_size_t, [c_int, c_int, c_int, c_int]),
     "hy_set_decode_kernel": (c_int, [c_int, c_int]),
+    "hy_set_decode_coresident": (c_int, [c_int]),
     "hy_attn_prefill_paged": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
                                       c_int, c_int, c_int, c_int, c_void_p, c_int, c_void_p,
                                       c_longlong, c_float, c_void_p, c_int, c_void_p]),

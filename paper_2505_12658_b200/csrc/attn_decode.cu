@@ -712,6 +712,285 @@ __global__ void __launch_bounds__(32 * NW)
   }
 }
 
+// K8c: decode attention built to share every SM with a tensor-bound GEMM of another row
+// group (co-resident mode, decode / prefill split).  Three things make it fit beside a
+// GEMM CTA (181.5 KB of shared memory, 46 K registers) and still pull bytes:
+//  * the KV stream lands in a small explicit shared-memory ring through bulk copies
+//    (cp.async.bulk, one 256-byte token row per lane, rows padded to 272 bytes so ldmatrix
+//    is conflict-free) -- not through L1, which a GEMM's maximum carveout shrinks to 28 KB;
+//  * S = Q K^T and O += P V run on mma.sync m16n8k16 with the G query heads of a KV head as
+//    the tile rows (G = 1 for MHA: one useful row, but 32 MMAs per 16-token block instead of
+//    ~350 CUDA-core instructions), so one warp consumes ~4x more bytes per second;
+//  * at most ONE CTA per SM: a CTA that lands on an SM already holding one exits at once
+//    (per-SM flags), so two of them can never take the room a GEMM CTA needs.
+// Items (sequence, KV head, split) come from a ticket counter; each warp streams whole items
+// through its own ring (lane 0 issues, all lanes consume), block ids reloaded 32 at a time.
+// PAD = false (lab): the K and V tiles arrive as two 4 KB copies in the pool's own 256-byte
+// row layout (ldmatrix then has 8-way bank conflicts) -- to weigh the per-copy cost of the
+// TMA engine against the conflicts.
+template <int G, bool PAD = true>
+struct DcCfg {
+  static constexpr int LDS = PAD ? 136 : 128;            // row stride (bf16): 272 / 256 bytes
+  static constexpr int TILE = 16 * LDS * 2;              // one 16-token K or V tile
+  static constexpr int Q_BYTES = G * LDS * 2;
+  static constexpr int STAGE = 2 * TILE + Q_BYTES;       // K | V | q rows of the item
+};
+
+template <int G, int NW, int SPW, bool PAD = true>
+__global__ void __launch_bounds__(32 * NW)
+    attn_decode_co_kernel(const bf16* __restrict__ q, int ld_q, int n, int n_kv,
+                          const int* __restrict__ slots, const int* __restrict__ ctx_len,
+                          const int* __restrict__ block_table, int bt_stride,
+                          const bf16* __restrict__ kv, long long block_stride, float scale_log2,
+                          int bps, int nsplit, bf16* __restrict__ out, int ld_o,
+                          float* __restrict__ part, int* __restrict__ ctr) {
+  pdl_trigger();
+  constexpr int D = 128;
+  constexpr int STAGE = DcCfg<G, PAD>::STAGE;
+  constexpr int DC_LDS = DcCfg<G, PAD>::LDS, DC_TILE = DcCfg<G, PAD>::TILE;
+  extern __shared__ __align__(128) uint8_t dc_smem[];
+  __shared__ int s_dup;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* sm_flag = ctr + 256;
+  if (threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    s_dup = atomicCAS(sm_flag + (smid & 255), 0, 1) != 0 ? 1 : 0;
+  }
+  __syncthreads();
+  if (s_dup) {  // another CTA of this grid owns this SM: leave the room to the GEMM
+    if (threadIdx.x == 0 && atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+    return;
+  }
+  pdl_wait();
+  uint8_t* ring = dc_smem + (size_t)warp * SPW * STAGE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(dc_smem + (size_t)NW * SPW * STAGE) + warp * SPW;
+  int2* meta = reinterpret_cast<int2*>(dc_smem + (size_t)NW * SPW * STAGE + NW * SPW * 8) + warp * SPW;
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < SPW; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const int n_items = n * n_kv * nsplit;
+  const size_t tile_elems = (size_t)HY_KV_BLOCK_TOKENS * D;
+  const size_t v_off = (size_t)n_kv * tile_elems;
+
+  // ---- load cursor (warp-uniform)
+  int l_item = -1, l_b = 0, l_h = 0, l_blk = 0, l_end = 0, l_first = 0, l_base = 0, l_bid = 0;
+  const int* l_bt = nullptr;
+  int next_t = 0;
+  if (lane == 0) next_t = atomicAdd(ctr, 1);
+  next_t = __shfl_sync(0xffffffffu, next_t, 0);
+  bool exhausted = false;
+  auto advance_item = [&]() {
+    while (true) {
+      const int t = next_t;
+      if (t >= n_items) {
+        exhausted = true;
+        return;
+      }
+      int nt = 0;
+      if (lane == 0) nt = atomicAdd(ctr, 1);  // one ticket ahead
+      next_t = __shfl_sync(0xffffffffu, nt, 0);
+      const int sp = t / (n * n_kv);
+      const int r = t - sp * n * n_kv;
+      const int b = r / n_kv, h = r - b * n_kv;
+      const int nblk = (ctx_len[b] + HY_KV_BLOCK_TOKENS - 1) / HY_KV_BLOCK_TOKENS;
+      const int b0 = sp * bps, b1 = min(nblk, b0 + bps);
+      if (b0 >= b1) continue;
+      l_item = t;
+      l_b = b;
+      l_h = h;
+      l_blk = l_first = l_base = b0;
+      l_end = b1;
+      l_bt = block_table + (size_t)slots[b] * bt_stride;
+      l_bid = b0 + lane < b1 ? l_bt[b0 + lane] : 0;
+      return;
+    }
+  };
+  auto issue = [&](int st) {
+    if (!exhausted && l_blk >= l_end) advance_item();
+    const uint32_t sb = smem_u32(ring + (size_t)st * STAGE);
+    if (exhausted) {
+      if (lane == 0) {
+        meta[st] = make_int2(-1, 0);
+        mbar_arrive(&bar[st]);
+      }
+      return;
+    }
+    if (l_blk - l_base >= 32) {  // next 32 block ids
+      l_base += 32;
+      l_bid = l_base + lane < l_end ? l_bt[l_base + lane] : 0;
+    }
+    const int bid = __shfl_sync(0xffffffffu, l_bid, l_blk - l_base);
+    const bool first = l_blk == l_first;
+    if (lane == 0) {
+      meta[st] = make_int2(l_item, l_blk | (first ? (1 << 30) : 0));
+      fence_proxy_async_smem();  // the consumer's reads of this stage precede the refill
+      mbar_expect_tx(&bar[st], 2 * tile_elems * 2 + (first ? G * D * 2 : 0));
+    }
+    __syncwarp();  // expect_tx before any lane's copy can complete
+    if (PAD) {
+      // lanes 0-15: K rows, 16-31: V rows of this (block, KV head); 256 bytes each
+      const bf16* src = kv + (size_t)bid * block_stride + (size_t)l_h * tile_elems +
+                        (lane >> 4) * v_off + (size_t)(lane & 15) * D;
+      bulk_load_1d(sb + (lane >> 4) * DC_TILE + (lane & 15) * DC_LDS * 2, src, D * 2,
+                   smem_u32(&bar[st]), kEvictFirst);
+    } else if (lane < 2) {
+      const bf16* src = kv + (size_t)bid * block_stride + (size_t)l_h * tile_elems + lane * v_off;
+      bulk_load_1d(sb + lane * DC_TILE, src, (uint32_t)tile_elems * 2, smem_u32(&bar[st]),
+                   kEvictFirst);
+    }
+    if (first && lane < G)
+      bulk_load_1d(sb + 2 * DC_TILE + lane * DC_LDS * 2,
+                   q + (size_t)l_b * ld_q + (size_t)(l_h * G + lane) * D, D * 2,
+                   smem_u32(&bar[st]), kEvictFirst);
+    ++l_blk;
+  };
+
+#pragma unroll
+  for (int st = 0; st < SPW; ++st) issue(st);
+
+  // ---- consumer
+  const int r0 = lane >> 2;  // accumulator rows r0 (c0, c1) and r0 + 8 (c2, c3)
+  int c_item = -1, c_ctx = 0;
+  uint32_t qf[8][4];
+  float o[16][4];
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  auto finish = [&]() {
+    if (c_item < 0) return;
+    float L0 = l0 + __shfl_xor_sync(0xffffffffu, l0, 1);
+    L0 += __shfl_xor_sync(0xffffffffu, L0, 2);
+    const int sp = c_item / (n * n_kv);
+    const int r = c_item - sp * n * n_kv;  // = b * n_kv + h
+    if (r0 < G) {  // G <= 8: only the c0 / c1 rows carry heads
+      const int b = r / n_kv, h = r - b * n_kv;
+      const int hq = h * G + r0;
+      if (nsplit == 1) {
+        const float inv = L0 > 0.f ? 1.f / L0 : 0.f;
+        bf16* op = out + (size_t)b * ld_o + (size_t)hq * D + (lane & 3) * 2;
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          *reinterpret_cast<uint32_t*>(op + i * 8) = pack_bf16x2(o[i][0] * inv, o[i][1] * inv);
+      } else {
+        float* pp = part + (((size_t)b * n_kv * G + hq) * nsplit + sp) * (D + 2);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          *reinterpret_cast<float2*>(pp + i * 8 + (lane & 3) * 2) = make_float2(o[i][0], o[i][1]);
+        if ((lane & 3) == 0) {
+          pp[D] = m0;
+          pp[D + 1] = L0;
+        }
+      }
+    }
+  };
+  int st = 0;
+  uint32_t ph = 0;
+  while (true) {
+    mbar_wait(&bar[st], ph);
+    const int2 md = meta[st];
+    if (md.x < 0) break;
+    const uint32_t sb = smem_u32(ring + (size_t)st * STAGE);
+    if (md.x != c_item) {
+      finish();
+      c_item = md.x;
+      c_ctx = ctx_len[(md.x % (n * n_kv)) / n_kv];
+      m0 = m1 = -INFINITY;
+      l0 = l1 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      // q fragments (rows >= G zero): a0 (r0, k), a1 (r0 + 8, k), a2 (r0, k + 8), a3 (r0 + 8, k + 8)
+      const uint32_t qa = sb + 2 * DC_TILE + r0 * DC_LDS * 2 + (lane & 3) * 4;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        uint32_t x0 = 0, x2 = 0;
+        if (r0 < G) {
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x0) : "r"(qa + kk * 32));
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(x2) : "r"(qa + kk * 32 + 16));
+        }
+        qf[kk][0] = x0;
+        qf[kk][1] = 0u;
+        qf[kk][2] = x2;
+        qf[kk][3] = 0u;
+      }
+    }
+    const int jb = md.y & ((1 << 30) - 1);
+    const uint32_t cK = sb, cV = sb + DC_TILE;
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int key = (lane & 7) + (lane >> 4) * 8;
+      const int col = kk * 16 + ((lane >> 3) & 1) * 8;
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(cK + (key * DC_LDS + col) * 2, b0, b1, b2, b3);
+      mma_bf16_16816(s[0], qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b0, b1);
+      mma_bf16_16816(s[1], qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b2, b3);
+    }
+    float mx0 = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tok = jb * HY_KV_BLOCK_TOKENS + nt * 8 + (lane & 3) * 2 + e;
+        s[nt][e] = tok < c_ctx ? s[nt][e] * scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, s[nt][e]);
+      }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    const float mn0 = fmaxf(m0, mx0);  // finite: every block holds a valid token
+    const float cr0 = exp2f(m0 - mn0);
+    m0 = mn0;
+    float rs0 = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      s[nt][0] = exp2f(s[nt][0] - mn0);
+      s[nt][1] = exp2f(s[nt][1] - mn0);
+      rs0 += s[nt][0] + s[nt][1];
+    }
+    l0 = l0 * cr0 + rs0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      o[i][0] *= cr0;
+      o[i][1] *= cr0;
+    }
+    // P (rows 8-15 zero) as the A operand
+    const uint32_t a0 = pack_bf16x2(s[0][0], s[0][1]), a2 = pack_bf16x2(s[1][0], s[1][1]);
+#pragma unroll
+    for (int dp = 0; dp < 8; ++dp) {
+      const int key = (lane & 7) + ((lane >> 3) & 1) * 8;
+      const int col = dp * 16 + (lane >> 4) * 8;
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(cV + (key * DC_LDS + col) * 2, b0, b1, b2, b3);
+      mma_bf16_16816(o[2 * dp], a0, 0u, a2, 0u, b0, b1);
+      mma_bf16_16816(o[2 * dp + 1], a0, 0u, a2, 0u, b2, b3);
+    }
+    __syncwarp();  // every lane has read the stage before it is refilled
+    issue(st);
+    if (++st == SPW) {
+      st = 0;
+      ph ^= 1;
+    }
+  }
+  finish();
+  (void)m1;
+  (void)l1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    sm_flag[smid & 255] = 0;
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+}
+
 // KV splits per (sequence, KV head): enough CTAs for ~per_sm per SM.  GQA CTAs (G >= 4
 // query heads per KV head, tensor-core kernel) aim for 4 per SM -- each already does G
 // heads of work per byte, and fewer splits save the combine pass (Qwen2-VL 28/4, 256 x 660
@@ -735,7 +1014,7 @@ static int decode_splits(int n, int n_kv, int max_ctx, int G = 1) {
 using namespace hy;
 
 // Workspace: [ticket counters: 256 B, zero between launches][split-KV partials]
-static constexpr size_t kDecCtrBytes = 256;
+static constexpr size_t kDecCtrBytes = 2048;  // [0]: tickets, [1]: done; [256..511]: SM flags
 
 extern "C" size_t hy_attn_decode_workspace_bytes(int n, int n_heads, int head_dim, int max_ctx) {
   const int ns = decode_splits(n, n_heads, max_ctx);  // n_kv <= n_heads: upper bound
@@ -800,9 +1079,14 @@ static int launch_bulk(const bf16* q, int ld_q, int n, int n_heads, const int* s
     return e ? atoi(e) : 0;
   }();
   const int cps = env_cps > 0 ? env_cps : t_dec_coresident ? 1 : std::max(occ, 1);
-  const int grid = (int)std::max<long long>(
-      1, std::min<long long>((long long)num_sms() * std::min(cps, std::max(occ, 1)),
-                             ceil_div(items, NW)));
+  static const int env_grid = [] {
+    const char* e = getenv("HY_DECODE_BULK_GRID");  // lab: cap the CTA count (SM subsets)
+    return e ? atoi(e) : 0;
+  }();
+  long long g = std::min<long long>((long long)num_sms() * std::min(cps, std::max(occ, 1)),
+                                    ceil_div(items, NW));
+  if (env_grid > 0) g = std::min<long long>(g, env_grid);
+  const int grid = (int)std::max<long long>(1, g);
   int* ctr = reinterpret_cast<int*>(ws);
   float* part = reinterpret_cast<float*>(ws + kDecCtrBytes);
   HY_CUDA_RET(launch_pdl(kern, dim3(grid), dim3(32 * NW), (size_t)SMEM, stream, q, ld_q, n,
@@ -816,11 +1100,82 @@ static int launch_bulk(const bf16* q, int ld_q, int n, int n_heads, const int* s
   }
   return 0;
 }
+
+// Co-resident K8c launch: one CTA per SM at most (the kernel enforces it), whole sequences
+// per item unless that leaves fewer than ~4 items per warp.
+template <int G, int NW, int SPW, bool PAD = true>
+static int launch_co(const bf16* q, int ld_q, int n, int n_kv, const int* slots, const int* ctx,
+                     int max_ctx, const int* bt, int bt_stride, const bf16* kv,
+                     long long block_stride, float sl2, bf16* out, int ld_o, uint8_t* ws,
+                     size_t ws_bytes, cudaStream_t stream) {
+  constexpr int SMEM = NW * SPW * (DcCfg<G, PAD>::STAGE + 16);
+  auto kern = attn_decode_co_kernel<G, NW, SPW, PAD>;
+  HY_CUDA_RET(ensure_smem(kern, SMEM));
+  HY_CUDA_RET(ensure_max_carveout(kern));
+  const int max_blocks = std::max(1, ceil_div(max_ctx, HY_KV_BLOCK_TOKENS));
+  const int want = 4 * num_sms() * NW;
+  const int ns0 = std::max(
+      1, std::min(std::min(ceil_div(want, std::max(1, n * n_kv)), ceil_div(max_blocks, 4)), 64));
+  const int bps = ceil_div(max_blocks, ns0);
+  const int ns = ceil_div(max_blocks, bps);
+  const size_t need = kDecCtrBytes + (size_t)n * n_kv * G * ns * (128 + 2) * sizeof(float);
+  if (ns > 1 && need > ws_bytes) {
+    set_last_error("decode attention: workspace too small for the co-resident kernel");
+    return (int)cudaErrorInvalidValue;
+  }
+  const long long items = (long long)n * n_kv * ns;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(2LL * num_sms(), ceil_div(items, NW)));
+  int* ctr = reinterpret_cast<int*>(ws);
+  float* part = reinterpret_cast<float*>(ws + kDecCtrBytes);
+  HY_CUDA_RET(launch_pdl(kern, dim3(grid), dim3(32 * NW), (size_t)SMEM, stream, q, ld_q, n, n_kv,
+                         slots, ctx, bt, bt_stride, kv, block_stride, sl2, bps, ns, out, ld_o,
+                         part, ctr));
+  HY_LAUNCH_CHECK();
+  if (ns > 1) {
+    HY_CUDA_RET(launch_pdl(attn_decode_combine_kernel, dim3(n, n_kv * G), dim3(128), 0, stream,
+                           (const float*)part, n_kv * G, ns, out, ld_o));
+    HY_LAUNCH_CHECK();
+  }
+  return 0;
+}
+
+// co-resident kernel choice: HY_DECODE_CO=<nw>,<spw> (A/B), default 2 warps x 2 stages
+static int co_dispatch(int G, const bf16* q, int ld_q, int n, int n_kv, const int* slots,
+                       const int* ctx, int max_ctx, const int* bt, int bt_stride, const bf16* kv,
+                       long long block_stride, float sl2, bf16* out, int ld_o, uint8_t* ws,
+                       size_t ws_bytes, cudaStream_t stream) {
+  BulkCfg env{2, 2};
+  int pad = 1;
+  if (const char* e = getenv("HY_DECODE_CO")) sscanf(e, "%d,%d,%d", &env.nw, &env.spw, &pad);
+  if (!pad && G == 1 && env.nw == 4 && env.spw == 1)
+    return launch_co<1, 4, 1, false>(q, ld_q, n, n_kv, slots, ctx, max_ctx, bt, bt_stride, kv,
+                                     block_stride, sl2, out, ld_o, ws, ws_bytes, stream);
+  if (!pad && G == 1 && env.nw == 2 && env.spw == 2)
+    return launch_co<1, 2, 2, false>(q, ld_q, n, n_kv, slots, ctx, max_ctx, bt, bt_stride, kv,
+                                     block_stride, sl2, out, ld_o, ws, ws_bytes, stream);
+#define HY_CO(GG, NW, SPW)                                                                   \
+  if (G == GG && env.nw == NW && env.spw == SPW)                                             \
+    return launch_co<GG, NW, SPW>(q, ld_q, n, n_kv, slots, ctx, max_ctx, bt, bt_stride, kv,  \
+                                  block_stride, sl2, out, ld_o, ws, ws_bytes, stream);
+  HY_CO(1, 2, 2)
+  HY_CO(1, 4, 1)
+  HY_CO(1, 1, 4)
+  HY_CO(7, 2, 2)
+  HY_CO(7, 1, 4)
+#undef HY_CO
+  return -1;  // no co-resident instance: the caller uses the default kernel
+}
 }  // namespace hy
+
+extern "C" int hy_set_decode_coresident(int on) {
+  hy::decode_set_coresident(on ? 1 : 0);
+  return 0;
+}
 
 extern "C" int hy_set_decode_kernel(int nw, int spw) {
   const bool ok = nw == 0 || (nw == 1 && spw == 4) || (nw == 2 && spw >= 2 && spw <= 4) ||
-                  (nw == 4 && (spw == 1 || spw == 2));
+                  (nw == 4 && (spw == 1 || spw == 2 || spw == 6)) || (nw == 8 && spw == 3) ||
+                  (nw == 1 && spw == 5) || (nw == 5 && spw == 1);
   if (!ok) {
     set_last_error("hy_set_decode_kernel: unsupported warps / stages");
     return (int)cudaErrorInvalidValue;
@@ -839,6 +1194,16 @@ extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads,
   HY_CHECK_ARG(n_kv_heads > 0 && n_heads % n_kv_heads == 0, "heads");
   if (n <= 0) return 0;
   const int G = n_heads / n_kv_heads;
+  if (t_dec_coresident && t_dec_nw == 0 && !getenv("HY_DECODE_NOCO")) {
+    uint8_t* wsb = reinterpret_cast<uint8_t*>(workspace);
+    HY_CHECK_ARG(wsb != nullptr && workspace_bytes >= kDecCtrBytes, "decode workspace");
+    const int rc = co_dispatch(G, reinterpret_cast<const bf16*>(q), ld_q, n, n_kv_heads, slots,
+                               ctx, max_ctx, block_table, bt_stride,
+                               reinterpret_cast<const bf16*>(kv_layer), block_stride,
+                               scale * 1.4426950408889634f, reinterpret_cast<bf16*>(out), ld_o,
+                               wsb, workspace_bytes, stream);
+    if (rc >= 0) return rc;
+  }
   if (G == 1) {
     const BulkCfg bc = bulk_cfg();
     if (bc.nw > 0) {
@@ -859,6 +1224,10 @@ extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads,
       HY_BULK(2, 4)
       HY_BULK(4, 1)
       HY_BULK(4, 2)
+      HY_BULK(4, 6)
+      HY_BULK(8, 3)
+      HY_BULK(1, 5)
+      HY_BULK(5, 1)
 #undef HY_BULK
       set_last_error("decode attention: no bulk kernel for this warp / stage count");
       return (int)cudaErrorInvalidValue;

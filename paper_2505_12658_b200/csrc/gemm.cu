@@ -721,40 +721,36 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
 // release the accumulator on the leader's accumulator-empty barrier.  Each CTA's TMEM
 // holds its own 128 rows of the 256 x BN accumulator (double-buffered).
 // ---------------------------------------------------------------------------
-// The pair kernel's per-warp TMA-store staging: two 2 KB buffers (default), or one
-// (HY_PAIR_STG_BYTES=2048, co-resident lab builds: 16 KB less shared memory per CTA)
-#ifndef HY_PAIR_STG_BYTES
-#define HY_PAIR_STG_BYTES 4096
-#endif
-constexpr int kPairStgBytes = HY_PAIR_STG_BYTES;
-constexpr bool kPairStgDbl = kPairStgBytes >= 4096;
-
-template <int BN>
+// SLIM (co-resident mode): a 160 KB operand ring and one 2 KB TMA-store buffer per epilogue
+// warp -- 181.5 KB instead of 225 KB at BN = 256, which leaves ~44 KB of the SM's shared
+// memory to a co-resident decode-attention CTA (attn_decode.cu) while this GEMM runs.
+template <int BN, bool SLIM = false>
 struct GemmPairCfg {
   static constexpr int BK = 64;
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (HY_PAIR_SMEM_KB * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = ((SLIM ? 160 : HY_PAIR_SMEM_KB) * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int STG_BYTES = SLIM ? kStgBytes / 2 : kStgBytes;  // per epilogue warp
   static constexpr int SMEM_BYTES =
-      STAGES * STAGE_BYTES + kEpiWarps * kPairStgBytes + 1024 /*align*/ + 256 /*barriers*/;
+      STAGES * STAGE_BYTES + kEpiWarps * STG_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int THREADS = 64 + 32 * kEpiWarps;
 };
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool SLIM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const GemmArgs a) {
-  using C = GemmPairCfg<BN>;
+  using C = GemmPairCfg<BN, SLIM>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint8_t* stg_base = smem + C::STAGES * C::STAGE_BYTES;  // epilogue TMA-store buffers
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + kEpiWarps * kPairStgBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg_base + kEpiWarps * C::STG_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
@@ -952,8 +948,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
                          (((size_t)(cc * 2 + slot) * 2 + rank) * (BN / 32) + c) * 8 * 128 + lrow;
           }
           add_partials(v, srcs, ns, nb);
-          epi_chunk<EPI, false, kPairStgDbl>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32,
-                                             v, lane, smem_u32(stg_base) + (warp - 2) * kPairStgBytes,
+          epi_chunk<EPI, false, !SLIM>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32,
+                                       v, lane, smem_u32(stg_base) + (warp - 2) * C::STG_BYTES,
                                              &tmC, nst);
         }
       }
@@ -977,29 +973,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool SLIM>
 static int launch_pair(const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
                        const GemmArgs& a, int grid, cudaStream_t st) {
-  using C = GemmPairCfg<BN>;
-  HY_CUDA_RET(ensure_smem(gemm_pair_kernel<BN, EPI>, C::SMEM_BYTES));
+  using C = GemmPairCfg<BN, SLIM>;
+  auto kern = gemm_pair_kernel<BN, EPI, SLIM>;
+  HY_CUDA_RET(ensure_smem(kern, C::SMEM_BYTES));
+  // the maximum carveout, so the SM's shared-memory configuration does not change between a
+  // GEMM and a small-smem kernel sharing the SM (a 196 KB split would fit this CTA alone)
+  HY_CUDA_RET(ensure_max_carveout(kern));
   if (a.dbg & 2)
-    gemm_pair_kernel<BN, EPI><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tA, tB, tC, a);
+    kern<<<grid, C::THREADS, C::SMEM_BYTES, st>>>(tA, tB, tC, a);
   else
-    HY_CUDA_RET(launch_pdl(gemm_pair_kernel<BN, EPI>, dim3(grid), dim3(C::THREADS),
-                           C::SMEM_BYTES, st, tA, tB, tC, a));
+    HY_CUDA_RET(launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES, st, tA, tB, tC, a));
   HY_LAUNCH_CHECK();
   return 0;
 }
 
-template <int BN>
+template <int BN, bool SLIM>
 static int launch_pair_epi(int epi, const CUtensorMap& tA, const CUtensorMap& tB,
                            const CUtensorMap& tC, const GemmArgs& a, int grid, cudaStream_t st) {
   switch (epi) {
-    case EPI_BF16: return launch_pair<BN, EPI_BF16>(tA, tB, tC, a, grid, st);
-    case EPI_QGELU: return launch_pair<BN, EPI_QGELU>(tA, tB, tC, a, grid, st);
-    case EPI_GELU: return launch_pair<BN, EPI_GELU>(tA, tB, tC, a, grid, st);
-    case EPI_SWIGLU: return launch_pair<BN, EPI_SWIGLU>(tA, tB, tC, a, grid, st);
-    case EPI_F32: return launch_pair<BN, EPI_F32>(tA, tB, tC, a, grid, st);
+    case EPI_BF16: return launch_pair<BN, EPI_BF16, SLIM>(tA, tB, tC, a, grid, st);
+    case EPI_QGELU: return launch_pair<BN, EPI_QGELU, SLIM>(tA, tB, tC, a, grid, st);
+    case EPI_GELU: return launch_pair<BN, EPI_GELU, SLIM>(tA, tB, tC, a, grid, st);
+    case EPI_SWIGLU: return launch_pair<BN, EPI_SWIGLU, SLIM>(tA, tB, tC, a, grid, st);
+    case EPI_F32: return launch_pair<BN, EPI_F32, SLIM>(tA, tB, tC, a, grid, st);
     default: return -1;
   }
 }
@@ -1009,6 +1008,7 @@ static int launch_gemm(const CUtensorMap& tA, const CUtensorMap& tB, const CUten
                        const GemmArgs& a, int grid, cudaStream_t st) {
   using C = GemmCfg<BN>;
   HY_CUDA_RET(ensure_smem(gemm_tc_kernel<BN, SWAP, EPI>, C::SMEM_BYTES));
+  HY_CUDA_RET(ensure_max_carveout(gemm_tc_kernel<BN, SWAP, EPI>));  // see launch_pair
   HY_CUDA_RET(launch_pdl(gemm_tc_kernel<BN, SWAP, EPI>, dim3(grid), dim3(C::THREADS), C::SMEM_BYTES,
                          st, tA, tB, tC, a));
   HY_LAUNCH_CHECK();
@@ -1047,6 +1047,9 @@ static constexpr size_t kCounterBytes = 16384;
 // SMs a GEMM grid may occupy (HY_GEMM_SMS caps it, e.g. to leave SMs to a concurrent stream)
 static thread_local int t_sms_cap = 0;  // per-thread cap (split-mode forwards)
 void gemm_set_sms_cap(int sms) { t_sms_cap = sms; }
+// co-resident mode (per host thread): pair GEMMs use the SLIM instance
+static thread_local int t_slim = 0;
+void gemm_set_coresident(int on) { t_slim = on; }
 
 static int gemm_sms() {
   static const int env_cap = [] {
@@ -1194,8 +1197,11 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     HY_RET_IF(make_tmap_2d_bf16(&tB, W, N, K, (uint64_t)ldw * 2, pair_bn / 2, 64));
     CUtensorMap tC = tA;
     HY_RET_IF(out_tmap(&tC, e, M, out_cols, a));
-    const int rc = pair_bn == 128 ? launch_pair_epi<128>(epi, tA, tB, tC, a, grid, st)
-                                  : launch_pair_epi<256>(epi, tA, tB, tC, a, grid, st);
+    const bool slim = t_slim || getenv("HY_GEMM_SLIM") != nullptr;
+    const int rc = pair_bn == 128 ? (slim ? launch_pair_epi<128, true>(epi, tA, tB, tC, a, grid, st)
+                                          : launch_pair_epi<128, false>(epi, tA, tB, tC, a, grid, st))
+                                  : (slim ? launch_pair_epi<256, true>(epi, tA, tB, tC, a, grid, st)
+                                          : launch_pair_epi<256, false>(epi, tA, tB, tC, a, grid, st));
     if (rc < 0) {
       set_last_error("gemm: no pair kernel for this epilogue");
       return (int)cudaErrorInvalidValue;

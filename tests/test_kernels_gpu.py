@@ -255,6 +255,56 @@ def test_decode_attention_bulk(cfg, ctxs):
         assert (outs[0][i].float() - ref).abs().max().item() < 2e-2, (i, c)
 
 
+@pytest.mark.parametrize("co", ["2,2", "4,1", "1,4"])
+@pytest.mark.parametrize("n_heads,n_kv,ctxs", [
+    (8, 8, [1, 17, 300, 33, 616, 617, 2000]),
+    (8, 8, [16 * 64 * 3 + 5, 15, 16]),         # long context
+    (8, 8, list(range(1, 400, 7))),            # many items per warp
+    (28, 4, [5, 900, 4097, 33]),               # GQA group 7 (Qwen2-VL)
+    (32, 32, [700] * 40),                      # LLaVA heads
+])
+def test_decode_attention_coresident(co, n_heads, n_kv, ctxs, monkeypatch):
+    """K8c (co-resident tensor-core decode kernel) vs the fp32 reference, twice on one
+    workspace (tickets and per-SM flags must be reset by the first call)."""
+    if co == "4,1" and n_heads // n_kv != 1:
+        pytest.skip("no GQA-7 instance with 4 warps")
+    monkeypatch.setenv("HY_DECODE_CO", co)
+    d, L, layer = 128, 2, 1
+    n = len(ctxs)
+    kv, bt, bts, be = _paged_setup(n, ctxs, n_kv, d, L, layer)
+    q = torch.randn(n, n_heads * d, device=DEV).bfloat16()
+    slots = torch.arange(n, device=DEV, dtype=torch.int32)
+    ctx = torch.tensor(ctxs, device=DEV, dtype=torch.int32)
+    wsb = lib().hy_attn_decode_workspace_bytes(n, n_heads, d, max(ctxs))
+    ws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=DEV)
+    layer_ptr = kv.data_ptr() + layer * 2 * n_kv * 16 * d * 2
+    outs = []
+    ck(lib().hy_set_decode_coresident(1), "coresident")
+    try:
+        for _ in range(2):
+            out = torch.empty(n, n_heads * d, device=DEV, dtype=torch.bfloat16)
+            ck(lib().hy_attn_decode_paged(q.data_ptr(), n_heads * d, n, n_heads, n_kv, d,
+                                          slots.data_ptr(), ctx.data_ptr(), max(ctxs),
+                                          bt.data_ptr(), bts, layer_ptr, be, 1 / math.sqrt(d),
+                                          out.data_ptr(), n_heads * d, ws.data_ptr(), ws.numel(),
+                                          st()), "decode co-resident")
+            outs.append(out)
+    finally:
+        lib().hy_set_decode_coresident(0)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    assert ws[:8].view(torch.int32).tolist() == [0, 0]
+    assert int(ws[1024:2048].view(torch.int32).abs().sum()) == 0  # per-SM flags released
+    grp = n_heads // n_kv
+    for i, c in enumerate(ctxs):
+        K, V = _gather_kv(kv, bt, i, c, L, layer, n_kv, d)
+        qi = q[i].float().view(n_heads, d)
+        Kx, Vx = K.repeat_interleave(grp, 1), V.repeat_interleave(grp, 1)
+        s = torch.einsum("hd,thd->ht", qi, Kx) / math.sqrt(d)
+        ref = torch.einsum("ht,thd->hd", torch.softmax(s, -1), Vx).reshape(-1)
+        assert (outs[0][i].float() - ref).abs().max().item() < 2e-2, (i, c)
+
+
 @pytest.mark.parametrize("n_heads,n_kv,chunks", [
     (4, 4, [(0, 70), (100, 37), (16, 64)]),           # (offset, chunk)
     (32, 32, [(0, 616)]),

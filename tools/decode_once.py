@@ -10,6 +10,8 @@ from paper_2505_12658_b200 import _lib  # noqa: E402
 
 nh, nkv, n, ctx = (int(x) for x in sys.argv[1:5])
 lib = _lib.load()
+if os.environ.get("HY_CO"):  # co-resident kernel (K8c)
+    lib.hy_set_decode_coresident(1)
 d = 128
 nb = -(-ctx // 16)
 be = 2 * nkv * 16 * d

@@ -25,6 +25,10 @@ def main():
     ap.add_argument("--seqs", type=int, default=400)
     ap.add_argument("--ctx", type=int, default=700)
     ap.add_argument("--bulk", default="0,0", help="decode kernel: nw,spw of the bulk kernel (0,0 = K8)")
+    ap.add_argument("--co", action="store_true", help="co-resident decode kernel (K8c)")
+    ap.add_argument("--delay", type=int, default=0,
+                    help="spin cycles on the attention stream before its launch, so the GEMM's "
+                    "CTAs are resident first")
     args = ap.parse_args()
     if args.lib:
         os.environ["HY_LIB_PATH"] = args.lib
@@ -33,6 +37,7 @@ def main():
     lib = _lib.load()
     nw, spw = (int(x) for x in args.bulk.split(","))
     assert lib.hy_set_decode_kernel(nw, spw) == 0, lib.hy_last_error()
+    lib.hy_set_decode_coresident(1 if args.co else 0)
     dev = "cuda:0"
     M, N, K = args.M, 12288, 4096
     A = torch.randn(M, K, device=dev).bfloat16()
@@ -83,6 +88,9 @@ def main():
         s1.wait_stream(cur)
         s2.wait_stream(cur)
         gemm(s1)
+        if args.delay:
+            with torch.cuda.stream(s2):
+                torch.cuda._sleep(args.delay)
         attn(s2)
         cur.wait_stream(s1)
         cur.wait_stream(s2)
@@ -92,7 +100,8 @@ def main():
     ta = timed(lambda: attn(cur))
     tb = timed(both)
     kv_bytes = n * ctx * 2 * nh * d * 2
-    print(f"lib {os.path.basename(_lib.LIB_PATH)} bulk {args.bulk} M={M}: gemm {tg:.1f} us "
+    print(f"lib {os.path.basename(_lib.LIB_PATH)} bulk {args.bulk} co {int(args.co)} "
+          f"slim {os.environ.get('HY_GEMM_SLIM', 0)} M={M}: gemm {tg:.1f} us "
           f"({2 * M * N * K / tg / 1e6:.0f} TF/s) | decode attn {n}x{ctx} {ta:.1f} us "
           f"({kv_bytes / ta / 1e3:.0f} GB/s) | both {tb:.1f} us (sum {tg + ta:.1f}, "
           f"max {max(tg, ta):.1f}, overlap {(tg + ta - tb) / min(tg, ta):.0%})", flush=True)
