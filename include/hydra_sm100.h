@@ -133,9 +133,9 @@ int hy_rope_kv_append(void* qkv, int ld_qkv, int rows, int n_heads, int n_kv_hea
 
 /* ---------------- K8: paged-KV decode attention ---------------- */
 /* q: [n, ld_q] (q heads x d at column 0); ctx[i] keys of slot slots[i]; out [n, ld_o].
- * workspace (hy_attn_decode_workspace_bytes): 256 B of ticket counters, then the split-KV
- * partials; it must be ZERO before its first use and every call leaves the counters zero
- * again (like the GEMM workspace).  Calls on different streams need different workspaces. */
+ * workspace (hy_attn_decode_workspace_bytes): 2 KB of ticket counters / per-SM flags (the
+ * opt-in K8b / K8c kernels reset them on the stream before each launch), then the split-KV
+ * partials.  Calls on different streams need different workspaces. */
 int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads, int n_kv_heads,
                          int head_dim, const int* slots, const int* ctx, int max_ctx,
                          const int* block_table, int bt_stride, const void* kv_layer,

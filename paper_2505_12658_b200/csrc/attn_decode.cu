@@ -558,7 +558,11 @@ __global__ void __launch_bounds__(32 * NW)
       const int b = r / n_heads, h = r - b * n_heads;
       const int nblk = (ctx_len[b] + HY_KV_BLOCK_TOKENS - 1) / HY_KV_BLOCK_TOKENS;
       const int b0 = sp * bps, b1 = min(nblk, b0 + bps);
-      if (b0 >= b1) continue;  // empty split of a short sequence
+      if (b0 >= b1) {  // empty split of a short sequence: an empty partial for the combine
+        float* pp = part + ((size_t)r * nsplit + sp) * (D + 2);
+        for (int i = lane; i < D + 2; i += 32) pp[i] = i == D ? -INFINITY : 0.f;
+        continue;
+      }
       l_item = t;
       l_b = b;
       l_h = h;
@@ -801,7 +805,13 @@ __global__ void __launch_bounds__(32 * NW)
       const int b = r / n_kv, h = r - b * n_kv;
       const int nblk = (ctx_len[b] + HY_KV_BLOCK_TOKENS - 1) / HY_KV_BLOCK_TOKENS;
       const int b0 = sp * bps, b1 = min(nblk, b0 + bps);
-      if (b0 >= b1) continue;
+      if (b0 >= b1) {  // empty split: empty partials (M = -inf, L = 0) for the combine
+        for (int g = 0; g < G; ++g) {
+          float* pp = part + (((size_t)b * n_kv * G + h * G + g) * nsplit + sp) * (D + 2);
+          for (int i = lane; i < D + 2; i += 32) pp[i] = i == D ? -INFINITY : 0.f;
+        }
+        continue;
+      }
       l_item = t;
       l_b = b;
       l_h = h;
@@ -1089,6 +1099,9 @@ static int launch_bulk(const bf16* q, int ld_q, int n, int n_heads, const int* s
   const int grid = (int)std::max<long long>(1, g);
   int* ctr = reinterpret_cast<int*>(ws);
   float* part = reinterpret_cast<float*>(ws + kDecCtrBytes);
+  // the counters start at zero on every call: a caller's workspace may move between calls
+  // (hy_lang_forward carves it per batch), so a reset left by the previous launch is not enough
+  HY_CUDA_RET(cudaMemsetAsync(ws, 0, kDecCtrBytes, stream));
   HY_CUDA_RET(launch_pdl(kern, dim3(grid), dim3(32 * NW), (size_t)SMEM, stream, q, ld_q, n,
                          n_heads, slots, ctx, bt, bt_stride, kv, block_stride, sl2, bps, ns, out,
                          ld_o, part, ctr));
@@ -1127,6 +1140,7 @@ static int launch_co(const bf16* q, int ld_q, int n, int n_kv, const int* slots,
   const int grid = (int)std::max<long long>(1, std::min<long long>(2LL * num_sms(), ceil_div(items, NW)));
   int* ctr = reinterpret_cast<int*>(ws);
   float* part = reinterpret_cast<float*>(ws + kDecCtrBytes);
+  HY_CUDA_RET(cudaMemsetAsync(ws, 0, kDecCtrBytes, stream));  // see launch_bulk
   HY_CUDA_RET(launch_pdl(kern, dim3(grid), dim3(32 * NW), (size_t)SMEM, stream, q, ld_q, n, n_kv,
                          slots, ctx, bt, bt_stride, kv, block_stride, sl2, bps, ns, out, ld_o,
                          part, ctr));

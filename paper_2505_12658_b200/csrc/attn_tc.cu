@@ -72,6 +72,32 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   return d;
 }
 
+// 2^x for a pair on the FMA pipe (FA4's trick for a softmax bound by the 16-per-clock SFU):
+// x = n + f with n = round(x) from the 1.5 * 2^23 magic add, f in [-0.5, 0.5], 2^f by a
+// degree-3 fit (max relative error 1.4e-4, far below the bf16 rounding of P), and n added
+// to the exponent bits.  x is clamped at -127 (the result is then ~0, as P needs).
+// HY_ATTN_POLY of every 16 pairs in a 32-key chunk take this path, the rest ex2.approx.
+#ifndef HY_ATTN_POLY
+#define HY_ATTN_POLY 6
+#endif
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float& e0, float& e1) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  x0 = fmaxf(x0, -127.f);
+  x1 = fmaxf(x1, -127.f);
+  const uint64_t x2 = pk2(x0, x1);
+  const uint64_t t2 = fadd2(x2, pk2(kMagic, kMagic));      // magic + round(x)
+  const uint64_t r2 = fadd2(t2, pk2(-kMagic, -kMagic));    // round(x)
+  const uint64_t f2 = ffma2(r2, pk2(-1.f, -1.f), x2);      // x - round(x)
+  uint64_t p2 = ffma2(f2, pk2(0.05502927f, 0.05502927f), pk2(0.24225698f, 0.24225698f));
+  p2 = ffma2(f2, p2, pk2(0.69325305f, 0.69325305f));
+  p2 = ffma2(f2, p2, pk2(0.99995134f, 0.99995134f));
+  float p0, p1, t0, t1;
+  up2(p2, p0, p1);
+  up2(t2, t0, t1);
+  e0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  e1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
 struct TcAttnParams {
   const int* qstart;   // [n_seqs + 1] query rows of each sequence in the Q map
   const int* offset;   // paged: tokens cached before the chunk
@@ -79,6 +105,7 @@ struct TcAttnParams {
   const int* block_table;
   int bt_stride;
   int q_tiles;         // 256-row query-tile pairs per sequence in the grid
+  int n_seqs;
   int group;           // query heads per kv head
   int k_col0, v_col0;  // varlen: column of kv head 0's K / V in the packed QKV map
   long long rows_per_block;  // paged: KV-map rows per cache block (block_stride / d)
@@ -116,11 +143,14 @@ __global__ void __launch_bounds__(64 + 256, 1)
                    const TcAttnParams p) {
   using C = TcAttnCfg<D, T>;
   pdl_wait();  // Q (and for varlen K/V) are written by the previous kernel on the stream
-  const int seq = blockIdx.x / p.q_tiles;
-  // pair of 128-row query tiles, last pair first: under the causal mask later pairs see more
-  // keys, so the heavy CTAs start in the first wave and the light ones fill the tail
-  const int qp = p.q_tiles - 1 - blockIdx.x % p.q_tiles;
-  const int h = blockIdx.y;
+  // grid (heads, q-tile pairs x sequences), heads fastest: the hardware launches CTAs in
+  // blockIdx order, so every head's LAST query-tile pair (the most keys under the causal
+  // mask) starts before any lighter pair -- longest-first over the whole grid, the light
+  // CTAs fill the tail (a 2304-token chunk: 288 CTAs on 148 SMs, SMs were busy 62% of the
+  // kernel with heads slowest)
+  const int seq = blockIdx.y % p.n_seqs;
+  const int qp = p.q_tiles - 1 - blockIdx.y / p.n_seqs;
+  const int h = blockIdx.x;
   const int kvh = h / p.group;
   const int q0 = p.qstart[seq];
   const int nq = p.qstart[seq + 1] - q0;
@@ -130,6 +160,10 @@ __global__ void __launch_bounds__(64 + 256, 1)
   const int kv_len = off + nq;
   const int kv_end = PAGED ? min(kv_len, off + qbase + C::TILES * C::BQ) : kv_len;
   const int n_kt = (kv_end + C::BK - 1) / C::BK;
+  // the pair's second tile holds no query row (a sequence's last, partial pair): it is
+  // skipped -- no Q K^T / P V issued, its softmax warps idle (e.g. a 577-token image: 5 of
+  // 6 tiles computed instead of 6)
+  const bool t1_live = T == 2 && qbase + C::BQ < nq;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -298,11 +332,12 @@ __global__ void __launch_bounds__(64 + 256, 1)
       tc_fence_after();
       if constexpr (T == 2) {
       issue_s(0, 0);
-      issue_s(1, 0);
+      if (t1_live) issue_s(1, 0);
       umma_commit(&k_empty[0]);  // K_0 retired once both Q K^T complete
       for (int j = 0; j < n_kt; ++j) {
         const bool more = j + 1 < n_kt;
         for (int t = 0; t < C::TILES; ++t) {
+          if (t == 1 && !t1_live) continue;
           issue_pv(t, j);
           if (more) {
             if (t == 0) {  // the next key tile is needed only from here on
@@ -365,7 +400,8 @@ __global__ void __launch_bounds__(64 + 256, 1)
     const int qrow = qbase + t * C::BQ + row;  // query row within the sequence
     const int qpos = off + qrow;               // absolute position of this query
     float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kt; ++j) {
+    const bool live = t == 0 || t1_live;
+    for (int j = 0; j < (live ? n_kt : 0); ++j) {
       mbar_wait(&s_full[t], j & 1);
       if (threadIdx.x == 64) ATR(4, j);
       tc_fence_after();
@@ -431,8 +467,13 @@ __global__ void __launch_bounds__(64 + 256, 1)
           const int k0 = c * 32 + 2 * u;
           float x0, x1;
           up2(ffma2(pk2(__uint_as_float(r[k0]), __uint_as_float(r[k0 + 1])), sc2, nms2), x0, x1);
-          float e0 = ex2_approx(x0);
-          float e1 = ex2_approx(x1);
+          float e0, e1;
+          if (u < HY_ATTN_POLY) {
+            exp2_poly2(x0, x1, e0, e1);
+          } else {
+            e0 = ex2_approx(x0);
+            e1 = ex2_approx(x1);
+          }
           if (!full) {
             e0 = kbase + k0 < kmax ? e0 : 0.f;
             e1 = kbase + k0 + 1 < kmax ? e1 : 0.f;
@@ -454,11 +495,11 @@ __global__ void __launch_bounds__(64 + 256, 1)
       if (threadIdx.x == 64) ATR(5, j);
     }
     // O_t / l -> global
-    mbar_wait(&o_done[t], (n_kt - 1) & 1);
+    if (live) mbar_wait(&o_done[t], (n_kt - 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll 1
-    for (int c = 0; c < (DV + 31) / 32; ++c) {
+    for (int c = 0; c < (live ? (DV + 31) / 32 : 0); ++c) {
       uint32_t o[32];
       tmem_ld_32x32b_x32(tO + c * 32, o);
       tmem_ld_wait();
@@ -551,8 +592,13 @@ __global__ void __launch_bounds__(64 + 256, 1)
           const int k0 = c * 32 + 2 * u;
           float x0, x1;
           up2(ffma2(pk2(__uint_as_float(r[k0]), __uint_as_float(r[k0 + 1])), sc2, nms2), x0, x1);
-          float e0 = ex2_approx(x0);
-          float e1 = ex2_approx(x1);
+          float e0, e1;
+          if (u < HY_ATTN_POLY) {
+            exp2_poly2(x0, x1, e0, e1);
+          } else {
+            e0 = ex2_approx(x0);
+            e1 = ex2_approx(x1);
+          }
           if (!full) {
             e0 = kbase + k0 < kmax ? e0 : 0.f;
             e1 = kbase + k0 + 1 < kmax ? e1 : 0.f;
@@ -611,8 +657,10 @@ static int launch_tc_attn(const CUtensorMap& tq, const CUtensorMap& tkv, const T
                           int n_seqs, int n_heads, cudaStream_t st) {
   using C = TcAttnCfg<D, T>;
   HY_CUDA_RET(ensure_smem(attn_tc_kernel<D, PAGED, T, DV>, C::SMEM));
-  HY_CUDA_RET(launch_pdl(attn_tc_kernel<D, PAGED, T, DV>, dim3(n_seqs * p.q_tiles, n_heads),
-                         dim3(C::THREADS), C::SMEM, st, tq, tkv, p));
+  TcAttnParams pp = p;
+  pp.n_seqs = n_seqs;
+  HY_CUDA_RET(launch_pdl(attn_tc_kernel<D, PAGED, T, DV>, dim3(n_heads, n_seqs * p.q_tiles),
+                         dim3(C::THREADS), C::SMEM, st, tq, tkv, pp));
   HY_LAUNCH_CHECK();
   return 0;
 }

@@ -81,7 +81,8 @@ struct GemmArgs {
   int P, Q, K;    // MMA-M extent (rows of map A), MMA-N extent (rows of map B), reduction
   int np, nq, nkb;
   int t_dp;       // whole tiles [0, t_dp) round-robin (multiple of the grid when stream-K)
-  int dbg;        // bits: 1 no early PDL trigger, 2 no PDL launch (pair, HY_PAIR_DBG); 4 no residual prefetch
+  int dbg;        // bits: 1 no early PDL trigger, 2 no PDL launch (pair, HY_PAIR_DBG); 4 no residual
+                  // prefetch; 8 late PDL trigger (after the producer's last load, HY_PDL_LATE)
   int group;      // raster group of token tiles (0 = auto; HY_GEMM_GROUP tuning only)
   long long u_sk; // k-block units of tiles [t_dp, T), split evenly over the grid
   int M, N;       // logical GEMM shape (tokens, physical weight rows)
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
   // allocates TMEM before its griddepcontrol.wait; if it could start while a CTA of this
   // grid had not allocated yet, the two would wait on each other (this grid's CTA for the
   // columns, the dependent for this grid's completion).
-  pdl_trigger();
+  if (!(a.dbg & 8)) pdl_trigger();
 
   int su0, su1;
   const int nseg = cta_segments(a, cta, G, su0, su1);
@@ -556,6 +557,8 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
           }
         }
       }
+      // late trigger: dependents launch once every CTA has issued its last operand load
+      if (a.dbg & 8) pdl_trigger();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -785,7 +788,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (!(a.dbg & 1)) pdl_trigger();  // after both CTAs hold their TMEM: see gemm_tc_kernel
+  if (!(a.dbg & 9)) pdl_trigger();  // after both CTAs hold their TMEM: see gemm_tc_kernel
   int su0, su1;
   const int nseg = cta_segments(a, pair, npairs, su0, su1);  // data-parallel + stream-K
 
@@ -832,6 +835,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
           }
         }
       }
+      if (a.dbg & 8) pdl_trigger();  // late trigger (see gemm_tc_kernel)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
@@ -1044,6 +1048,16 @@ static int launch_epi(int epi, int bn, const CUtensorMap& tA, const CUtensorMap&
 // region must be zero before first use; every call leaves it zeroed again.
 static constexpr size_t kCounterBytes = 16384;
 
+// HY_PDL_LATE=1 (with HY_PDL=1): GEMMs release their dependents after the last operand load
+// instead of at entry, so an early dependent does not sit on SMs for the whole main loop
+static bool pdl_late() {
+  static const bool on = [] {
+    const char* e = getenv("HY_PDL_LATE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // SMs a GEMM grid may occupy (HY_GEMM_SMS caps it, e.g. to leave SMs to a concurrent stream)
 static thread_local int t_sms_cap = 0;  // per-thread cap (split-mode forwards)
 void gemm_set_sms_cap(int sms) { t_sms_cap = sms; }
@@ -1188,7 +1202,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     }
     // HY_PAIR_DBG=1: no early release of dependents (bisection aid; the serving hang it
     // isolated was a trigger issued before the TMEM allocation, see gemm_tc_kernel)
-    a.dbg = 0;
+    a.dbg = pdl_late() ? 8 : 0;
     if (const char* d = getenv("HY_PAIR_DBG")) a.dbg = atoi(d);
     if (getenv("HY_GEMM_NOPREF")) a.dbg |= 4;  // A/B: no residual L2 prefetch
     if (const char* g = getenv("HY_GEMM_GROUP")) a.group = atoi(g);
@@ -1221,6 +1235,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     a.Q = N;
   }
   if (const char* env_bn = getenv("HY_GEMM_BN")) bn = atoi(env_bn);  // tuning only
+  if (pdl_late()) a.dbg |= 8;
   if (getenv("HY_GEMM_NOPREF")) a.dbg |= 4;  // A/B: no residual L2 prefetch
   if (const char* g = getenv("HY_GEMM_GROUP")) a.group = atoi(g);
   a.np = ceil_div(a.P, 128);

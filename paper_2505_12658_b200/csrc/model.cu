@@ -17,6 +17,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
               const HyGemmEpilogue* e, void* ws, size_t ws_bytes, cudaStream_t st, int force_mode);
 void gemm_set_sms_cap(int sms);
 void decode_set_coresident(int on);
+void gemm_set_coresident(int on);
 int rmsnorm(const void* x, int ldx, const void* w, void* out, int ldo, int rows, int cols,
             float eps, const int* row_idx, cudaStream_t st);
 int layernorm(const void* x, int ldx, const void* w, const void* b, void* out, int ldo, int rows,
@@ -199,7 +200,13 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
     cudaEvent_t join = nullptr;
     HY_RET_IF(side_fork(st, &side, &join));
     int rc = 0;
-    decode_set_coresident(1);  // decode attention CTAs may share SMs with the other group's GEMMs
+    // HY_SPLIT_CO=1: decode attention as the co-resident kernel (K8c, one CTA per SM beside
+    // the prefill group's SLIM GEMMs).  Opt-in: measured, it pulls too few bytes per SM to
+    // pay (tools/lab/coresident.sh)
+    const char* ce = getenv("HY_SPLIT_CO");  // bits: 1 decode K8c, 2 SLIM GEMMs
+    const int co = ce ? atoi(ce) : 0;
+    decode_set_coresident(co & 1);
+    gemm_set_coresident((co >> 1) & 1);
     for (int li = 0; li < m->n_layers && rc == 0; ++li) {
       rc = layer(li, 0, 0, nd, nd, side, w.gemm_ws2, w.dec_ws);      // decode rows
       if (rc == 0) rc = layer(li, 1, 0, nd, nd, side, w.gemm_ws2, w.dec_ws);
@@ -207,6 +214,7 @@ extern "C" int hy_lang_forward(const HyLangModel* m, const HyLangBatch* b, const
       if (rc == 0) rc = layer(li, 1, nd, R, 0, st, w.gemm_ws, w.dec_ws2);
     }
     decode_set_coresident(0);
+    gemm_set_coresident(0);
     HY_RET_IF(rc);
     HY_RET_IF(side_join(st, side, join));
   } else if (split_min > 0 && nd >= split_min) {

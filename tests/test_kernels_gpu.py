@@ -229,7 +229,9 @@ def test_decode_attention_bulk(cfg, ctxs):
     slots = torch.arange(n, device=DEV, dtype=torch.int32)
     ctx = torch.tensor(ctxs, device=DEV, dtype=torch.int32)
     wsb = lib().hy_attn_decode_workspace_bytes(n, n_heads, d, max(ctxs))
-    ws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=DEV)
+    # garbage, not zeros: a caller's workspace may hold stale data (the kernel resets its
+    # counters and writes a partial for every split, empty ones included)
+    ws = torch.randint(0, 255, (max(wsb, 16),), dtype=torch.uint8, device=DEV)
     layer_ptr = kv.data_ptr() + layer * 2 * n_kv * 16 * d * 2
     outs = []
     ck(lib().hy_set_decode_kernel(*cfg), "set kernel")
@@ -276,7 +278,7 @@ def test_decode_attention_coresident(co, n_heads, n_kv, ctxs, monkeypatch):
     slots = torch.arange(n, device=DEV, dtype=torch.int32)
     ctx = torch.tensor(ctxs, device=DEV, dtype=torch.int32)
     wsb = lib().hy_attn_decode_workspace_bytes(n, n_heads, d, max(ctxs))
-    ws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=DEV)
+    ws = torch.randint(0, 255, (max(wsb, 16),), dtype=torch.uint8, device=DEV)  # see above
     layer_ptr = kv.data_ptr() + layer * 2 * n_kv * 16 * d * 2
     outs = []
     ck(lib().hy_set_decode_coresident(1), "coresident")

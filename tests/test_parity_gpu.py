@@ -226,10 +226,14 @@ def test_split_row_groups_parity(monkeypatch):
     assert res["tokens_equal"] + res["near_ties"] == res["rows"], res
 
 
-def test_split_decode_prefill_groups_parity(monkeypatch):
+@pytest.mark.parametrize("co", [None, "3"])
+def test_split_decode_prefill_groups_parity(co, monkeypatch):
     """HY_LANG_SPLIT_PD: decode rows and prefill rows run as two independent row groups on
-    two streams -- same scheduler decisions and logits as the one-stream path."""
+    two streams -- same scheduler decisions and logits as the one-stream path; co = "3":
+    the decode rows' attention on the co-resident kernel K8c beside SLIM GEMMs."""
     monkeypatch.setenv("HY_LANG_SPLIT_PD", "1")
+    if co:
+        monkeypatch.setenv("HY_SPLIT_CO", co)
     shape = get_shape("tiny")
     g, cl, _ = _run("config1_2000rps", shape)
     assert batch_log_digest(cl.batch_log) == g["sha"]

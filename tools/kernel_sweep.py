@@ -143,9 +143,11 @@ def attn_sweep(out):
         from flash_attn import flash_attn_varlen_func
     except Exception:  # noqa: BLE001
         flash_attn_varlen_func = None
-    # ViT: n images x 577 tokens, 16 heads x 64
-    for n_img in (1, 3, 8, 32):
-        nh, d, T = 16, 64, 577
+    # ViT: n images x T tokens: LLaVA 16 heads x 64 (577 tokens), Qwen2-VL 16 heads x 80
+    # (dynamic resolution)
+    for n_img, T, d in ((1, 577, 64), (3, 577, 64), (8, 577, 64), (32, 577, 64), (1, 2916, 80),
+                        (4, 1024, 80), (8, 576, 80)):
+        nh = 16
         tot = n_img * T
         qkv = torch.randn(tot, 3 * nh * d, device=DEV).bfloat16()
         o = torch.empty(tot, nh * d, device=DEV, dtype=torch.bfloat16)
@@ -165,11 +167,11 @@ def attn_sweep(out):
                 flash_attn_varlen_func(q, k, v, seg, seg, T, T)
             t1 = timeit(fa)
         fl = 4.0 * d * nh * n_img * T * T
-        r = {"name": "vit_attn", "images": n_img, "ours_us": t0 * 1e3,
+        r = {"name": "vit_attn", "images": n_img, "T": T, "d": d, "ours_us": t0 * 1e3,
              "ours_tflops": fl / t0 / 1e9, "fa_us": t1 * 1e3 if t1 else None,
              "fa_tflops": fl / t1 / 1e9 if t1 else None}
         out.append(r)
-        print(f"vit_attn images={n_img:3d}  ours {t0*1e3:8.1f} us {r['ours_tflops']:7.1f} TF | "
+        print(f"vit_attn images={n_img:3d} x {T:4d} d={d}  ours {t0*1e3:8.1f} us {r['ours_tflops']:7.1f} TF | "
               f"flash_attn {r['fa_us'] or 0:8.1f} us {r['fa_tflops'] or 0:7.1f} TF", flush=True)
     # prefill: chunks (offset, len) over paged KV, 32 heads x 128
     for chunks in ([(0, 616)], [(0, 616)] * 4, [(0, 1024), (1024, 1024)], [(0, 2304)]):
