@@ -58,7 +58,7 @@ __device__ __forceinline__ void trace(int i) {
 }
 // per-CTA marks: [cta][0] entry, [1] first full barrier, [2] last accumulator handed to the
 // epilogue, [3] exit, [4] segments, [5] stream-K tiles finished by this CTA
-__device__ unsigned long long g_ctr[160][6];
+__device__ unsigned long long g_ctr[160][10];
 __device__ __forceinline__ void cta_mark(int i) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -389,6 +389,31 @@ __device__ __forceinline__ void add_partials(float* v, const float4* const* srcs
   }
 }
 
+// One other contributor's 32-column chunk (8 float4 per lane) and the ordered add of exactly
+// one contributor -- the stream-K fixup's common case (a tile shared by two CTAs / pairs).
+// Loading the NEXT chunk before the current chunk's epilogue keeps one L2 round trip in
+// flight under the epilogue instead of paying one per chunk in series.
+__device__ __forceinline__ void ld_partial(float4* f, const float4* src) {
+#pragma unroll
+  for (int t = 0; t < 8; ++t) f[t] = __ldcg(src + t * 128);
+}
+__device__ __forceinline__ void add_one(float* v, const float4* f, bool other_first) {
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    if (other_first) {  // x_other + v  (same association as add_partials)
+      v[4 * t] = f[t].x + v[4 * t];
+      v[4 * t + 1] = f[t].y + v[4 * t + 1];
+      v[4 * t + 2] = f[t].z + v[4 * t + 2];
+      v[4 * t + 3] = f[t].w + v[4 * t + 3];
+    } else {
+      v[4 * t] += f[t].x;
+      v[4 * t + 1] += f[t].y;
+      v[4 * t + 2] += f[t].z;
+      v[4 * t + 3] += f[t].w;
+    }
+  }
+}
+
 // Stream-K: true when every other contributor of this tile has already published its
 // partial (arrival counter == others), checked only for a CTA's last segment (slot 1), the
 // one that normally completes last.  The acquire load orders the partial reads after the
@@ -526,9 +551,14 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
         const Seg sg = get_segment(a, cta, G, i, su0, su1);
         int p, q;
         raster_tile(sg.tile, a, p, q);
+        if (i == 0) HY_TR(13);
         for (int kb = sg.kb0; kb < sg.kb1 && npre < C::STAGES; ++kb, ++npre) {
           mbar_expect_tx(&full[npre], C::STAGE_BYTES);
           load_w(npre, kb, p, q);
+          // launched without PDL: nothing to wait for, the activations go out with the weights
+          // (the first stage lands ~1 us earlier than after the whole weight prologue)
+          if (a.dbg & 16) load_x(npre, kb, p, q);
+          if (npre == 0) HY_TR(14);
         }
       }
       HY_TR(2);
@@ -544,7 +574,7 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
         raster_tile(sg.tile, a, p, q);
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++g) {
           if (g < npre) {
-            load_x(stage, kb, p, q);
+            if (!(a.dbg & 16)) load_x(stage, kb, p, q);
           } else {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -613,7 +643,7 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
       const Seg sg = get_segment(a, cta, G, i, su0, su1);
       int p, q;
       raster_tile(sg.tile, a, p, q);
-      if (!SWAP && sg.slot < 0) prefetch_residual<BN, EPI>(a, p * 128 + sub * 32 + lane, q * BN, half);
+      if (!SWAP && sg.slot != 0) prefetch_residual<BN, EPI>(a, p * 128 + sub * 32 + lane, q * BN, half);
       mbar_wait_sleepy(&tfull[acc], acc_phase);
       if (i == 0 && threadIdx.x == 64) HY_TR(6);
       tc_fence_after();
@@ -811,7 +841,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
         const Seg sg = get_segment(a, pair, npairs, i, su0, su1);
         int p, q;
         raster_tile(sg.tile, a, p, q);
-        for (int kb = sg.kb0; kb < sg.kb1 && npre < C::STAGES; ++kb, ++npre) load_w(npre, kb, q);
+        for (int kb = sg.kb0; kb < sg.kb1 && npre < C::STAGES; ++kb, ++npre) {
+          load_w(npre, kb, q);
+          if (a.dbg & 16) load_x(npre, kb, p);  // no PDL: see gemm_tc_kernel
+        }
       }
       pdl_wait();
       int stage = 0;
@@ -823,7 +856,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
         raster_tile(sg.tile, a, p, q);
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++g) {
           if (g < npre) {
-            load_x(stage, kb, p);
+            if (!(a.dbg & 16)) load_x(stage, kb, p);
           } else {
             mbar_wait(&empty[stage], phase ^ 1);
             load_w(stage, kb, q);
@@ -891,8 +924,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
       const Seg sg = get_segment(a, pair, npairs, i, su0, su1);
       int p, q;
       raster_tile(sg.tile, a, p, q);
-      if (sg.slot < 0) prefetch_residual<BN, EPI>(a, p * 256 + rank * 128 + sub * 32 + lane, q * BN, half);
+      if (sg.slot != 0) prefetch_residual<BN, EPI>(a, p * 256 + rank * 128 + sub * 32 + lane, q * BN, half);
       mbar_wait_sleepy(&tfull[acc], acc_phase);
+      const bool mark = i == nseg - 1 && warp == 2 && lane == 0;
+      if (mark) HY_CM(6);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(sub * 32) << 16) + acc * BN;
       const int lrow = sub * 32 + lane;  // this CTA's accumulator row (TMEM lane)
@@ -930,7 +965,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
         if (finish && lane == 0 && sub == 0 && half == 0) HY_CINC(5);
         if (finish && lane == 0) *ctr = 0;
       }
-      if (finish) {
+      if (mark) HY_CM(7);
+      if (finish && sg.slot >= 0 && c1 - c0 == 1) {
+        // two contributors: the other's partial of the next chunk is loaded while this
+        // chunk's epilogue runs (one L2 round trip in flight, not one per chunk in series)
+        const int other = c0 == pair ? c1 : c0;
+        const long long cu0 = (long long)other * a.u_sk / npairs;
+        const float4* obase = reinterpret_cast<const float4*>(a.partial) +
+                              ((size_t)(other * 2 + (cu0 >= ub ? 0 : 1)) * 2 + rank) * (BN / 32) *
+                                  8 * 128 + lrow;
+        float4 fa[8], fb[8];
+        ld_partial(fa, obase + (size_t)half * 8 * 128);
+#pragma unroll
+        for (int c = half; c < BN / 32; c += 2) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + c * 32, r);
+          if (c + 2 < BN / 32) ld_partial(fb, obase + (size_t)(c + 2) * 8 * 128);
+          tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          add_one(v, fa, other < pair);
+          epi_chunk<EPI, false, !SLIM>(a, p * 256 + rank * 128 + sub * 32, q * BN + c * 32,
+                                       v, lane, smem_u32(stg_base) + (warp - 2) * C::STG_BYTES,
+                                       &tmC, nst);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) fa[t] = fb[t];
+        }
+      } else if (finish) {
 #pragma unroll 1
         for (int c = half; c < BN / 32; c += 2) {
           uint32_t r[32];
@@ -957,6 +1019,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * kEpiWarps,
                                              &tmC, nst);
         }
       }
+      if (mark) HY_CM(8);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
@@ -1100,6 +1163,33 @@ static int out_tmap(CUtensorMap* tC, const HyGemmEpilogue* e, int M, int out_col
 // projections at M = 640-3600, tools/kernel_sweep.py.)
 static int sk_dp_tiles(int T, int G) { return T >= 2 * G ? (T / G - 1) * G : 0; }
 
+// Measured dispatch (tools/gemm_tune.py on a B200, generated into gemm_table.inc): for the
+// served models' (N, K) pairs, the fastest kernel configuration at a grid of token counts.
+// An entry covers M up to m_max (the grid point; entries of one (N, K) ascend in m_max).
+// Shapes outside the table use the wave heuristic below.
+struct GemmTableEntry {
+  int n, k, m_max;
+  int kind;  // 1 swap-AB, 2 single-CTA normal, 3 CTA pair
+  int bn;    // tile width (pair: 128 / 256; single / swap: 32-256)
+  int sk;    // stream-K: 0 off, 1 on
+};
+static const GemmTableEntry kGemmTable[] = {
+#include "gemm_table.inc"
+    {0, 0, 0, 0, 0, 0}};
+
+static const GemmTableEntry* gemm_table_lookup(int M, int N, int K) {
+  static const bool off = getenv("HY_GEMM_NOTABLE") != nullptr;
+  if (off) return nullptr;
+  const GemmTableEntry* last = nullptr;
+  for (const GemmTableEntry* e = kGemmTable; e->n; ++e) {
+    if (e->n != N || e->k != K) continue;
+    if (M <= e->m_max) return e;
+    last = e;
+  }
+  (void)last;  // beyond the measured range: the heuristic
+  return nullptr;
+}
+
 int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K,
               const HyGemmEpilogue* e, void* ws, size_t ws_bytes, cudaStream_t st, int force_mode) {
   HY_CHECK_ARG(M >= 0 && N > 0 && K > 0, "gemm shape");
@@ -1139,6 +1229,23 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
 
   if (force_mode == 0)
     if (const char* fm = getenv("HY_GEMM_MODE")) force_mode = atoi(fm);  // tuning only
+  // measured table (when no tuning override forces the mode)
+  int tab_bn = 0, tab_sk = -1;
+  if (force_mode == 0 && !getenv("HY_GEMM_BN") && !getenv("HY_PAIR_BN") && !t_slim) {
+    if (const GemmTableEntry* te = gemm_table_lookup(M, N, K)) {
+      if (te->kind == 3 && N % te->bn == 0 && N % 128 == 0) {
+        force_mode = 3;
+      } else if (te->kind == 2 && N % 128 == 0 && N % te->bn == 0) {
+        force_mode = 2;
+      } else if (te->kind == 1) {
+        force_mode = 1;
+      }
+      if (force_mode) {
+        tab_bn = te->bn;
+        tab_sk = te->sk;
+      }
+    }
+  }
   // CTA-pair kernel: large token counts, weight rows a multiple of 256
   // when it needs no more full waves than the single-CTA kernel (a pair tile takes about as
   // long on two SMs as a 128-row tile on one, so waves decide)
@@ -1170,6 +1277,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   } else if (force_mode == 3 && N % 256 != 0) {
     pair_bn = 128;
   }
+  if (pair && tab_bn) pair_bn = tab_bn;
   if (const char* e = getenv("HY_PAIR_BN")) pair_bn = atoi(e);  // tuning only
   if (pair) {
     HY_CHECK_ARG(N % pair_bn == 0, "pair kernel needs N % 128 == 0");
@@ -1185,8 +1293,9 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     // 69.8 us with, 54.8 us without; tools/kernel_sweep.py).
     const size_t need = kCounterBytes + (size_t)slots * 2 * 2 * 128 * pair_bn * sizeof(float);
     const double dp_eff = (double)T / ((double)ceil_div(T, slots) * slots);
+    const bool want_sk = tab_sk >= 0 ? tab_sk == 1 : getenv("HY_PAIR_SK") != nullptr;
     bool sk = ws != nullptr && ws_bytes >= need && dp_eff < 0.9 && a.nkb >= 16 &&
-              (long long)T * a.nkb < (1LL << 31) && getenv("HY_PAIR_SK") != nullptr;
+              (long long)T * a.nkb < (1LL << 31) && want_sk;
     int grid;
     if (!sk) {
       grid = 2 * std::min(T, slots);
@@ -1204,6 +1313,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     // isolated was a trigger issued before the TMEM allocation, see gemm_tc_kernel)
     a.dbg = pdl_late() ? 8 : 0;
     if (const char* d = getenv("HY_PAIR_DBG")) a.dbg = atoi(d);
+    if (!pdl_enabled() || (a.dbg & 2)) a.dbg |= 16;  // no PDL launch: early activation loads
     if (getenv("HY_GEMM_NOPREF")) a.dbg |= 4;  // A/B: no residual L2 prefetch
     if (const char* g = getenv("HY_GEMM_GROUP")) a.group = atoi(g);
     CUtensorMap tA, tB;
@@ -1234,8 +1344,10 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     a.P = M;
     a.Q = N;
   }
+  if (tab_bn) bn = tab_bn;
   if (const char* env_bn = getenv("HY_GEMM_BN")) bn = atoi(env_bn);  // tuning only
   if (pdl_late()) a.dbg |= 8;
+  if (!pdl_enabled()) a.dbg |= 16;  // no PDL launch: early activation loads
   if (getenv("HY_GEMM_NOPREF")) a.dbg |= 4;  // A/B: no residual L2 prefetch
   if (const char* g = getenv("HY_GEMM_GROUP")) a.group = atoi(g);
   a.np = ceil_div(a.P, 128);
@@ -1254,6 +1366,8 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   bool sk = ws != nullptr && ws_bytes >= need && units_fit &&
             (swap ? (a.nkb >= 4 && (T > sms ? dp_eff < 0.85 : dp_eff < 0.5))
                   : (dp_eff < 0.5 && a.nkb >= 32));
+  if (tab_sk == 0) sk = false;
+  if (tab_sk == 1) sk = ws != nullptr && ws_bytes >= need && units_fit;
   if (getenv("HY_GEMM_NOSK")) sk = false;
   if (getenv("HY_GEMM_SK")) sk = ws != nullptr && ws_bytes >= need && units_fit;
   int grid;

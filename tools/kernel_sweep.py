@@ -283,11 +283,14 @@ def overlap_probe(out):
 def decode_sweep(out):
     """Paged decode attention (K8) bandwidth for MHA (LLaVA) and GQA (Qwen2-VL 28/4)."""
     import math
-    for nh, nkv, n, ctx, shuffled in ((32, 32, 256, 660, 0), (32, 32, 256, 660, 1),
-                                      (32, 32, 128, 700, 1), (32, 32, 64, 700, 1),
-                                      (32, 32, 32, 700, 1), (28, 4, 256, 660, 0),
-                                      (28, 4, 64, 4000, 0), (32, 8, 256, 660, 0),
-                                      (32, 32, 16, 8000, 0)):
+    shapes = ((32, 32, 256, 660, 0), (32, 32, 256, 660, 1), (32, 32, 128, 700, 1),
+              (32, 32, 64, 700, 1), (32, 32, 32, 700, 1), (28, 4, 256, 660, 0),
+              (28, 4, 64, 4000, 0), (32, 8, 256, 660, 0), (32, 32, 16, 8000, 0))
+    if os.environ.get("DECODE_SHAPES"):  # "nh/nkv/seqs/ctx/shuffled;..."
+        shapes = [tuple(int(v) for v in x.split("/")) for x in os.environ["DECODE_SHAPES"].split(";")]
+    if os.environ.get("DECODE_CO"):
+        lib().hy_set_decode_coresident(1)
+    for nh, nkv, n, ctx, shuffled in shapes:
         d = 128
         nb = -(-ctx // 16)
         be = 2 * nkv * 16 * d

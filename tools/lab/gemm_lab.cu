@@ -56,7 +56,7 @@ int main(int argc, char** argv) {
       printf("   trace:");
       for (int i = 1; i < 16; ++i) printf(" %d:%lld", i, (long long)(tr[i] - tr[0]));
       {
-        unsigned long long cm[160][6];
+        unsigned long long cm[160][10];
         cudaMemcpyFromSymbol(cm, hy::g_ctr, sizeof(cm));
         unsigned long long t0 = ~0ull, tfirst_max = 0, tend_max = 0, tmma_max = 0;
         const int nc = 148;
@@ -66,16 +66,18 @@ int main(int argc, char** argv) {
           if (!cm[c][0] || cm[c][0] < t0) continue;
           if (cm[c][3] - t0 > 1000000000ull) continue;
           if (c < 8 || c % 10 == 0)
-            printf(" [%d %lld/%lld/%lld/%lld s%lld f%lld]", c, (long long)(cm[c][0] - t0),
+            printf(" [%d %lld/%lld/%lld/%lld s%lld e%lld/%lld/%lld]", c, (long long)(cm[c][0] - t0),
                    cm[c][1] ? (long long)(cm[c][1] - t0) : -1LL, cm[c][2] ? (long long)(cm[c][2] - t0) : -1LL,
-                   (long long)(cm[c][3] - t0), (long long)cm[c][4], (long long)cm[c][5]);
+                   (long long)(cm[c][3] - t0), (long long)cm[c][4],
+                   cm[c][6] ? (long long)(cm[c][6] - t0) : -1LL, cm[c][7] ? (long long)(cm[c][7] - t0) : -1LL,
+                   cm[c][8] ? (long long)(cm[c][8] - t0) : -1LL);
           if (cm[c][1]) tfirst_max = std::max(tfirst_max, cm[c][1] - t0);
           if (cm[c][2]) tmma_max = std::max(tmma_max, cm[c][2] - t0);
           tend_max = std::max(tend_max, cm[c][3] - t0);
         }
         printf("\n   max first-full %lld  max last-mma %lld  max exit %lld\n", (long long)tfirst_max,
                (long long)tmma_max, (long long)tend_max);
-        static unsigned long long zero[160][6];
+        static unsigned long long zero[160][10];
         cudaMemcpyToSymbol(hy::g_ctr, zero, sizeof(zero));
       }
       printf("   MHz(0->8): %.0f  cycles 10->13: %lld 13->15: %lld\n", (double)(tr[24] - tr[16]) * 1e3 / (double)(tr[8] - tr[0]), (long long)(tr[29]-tr[26]), (long long)(tr[31]-tr[29]));
