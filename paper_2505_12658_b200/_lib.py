@@ -110,6 +110,7 @@ _SIGS = {
     "hy_device_sm_count": (c_int, []),
     "hy_launch_count": (c_longlong, []),
     "hy_set_kernel_timer": (None, [c_void_p]),
+    "hy_set_pdl": (c_int, [c_int]),
     "hy_gemm_bf16": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int,
                              POINTER(HyGemmEpilogue), c_void_p, c_size_t, c_void_p]),
     "hy_gemm_bf16_mode": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int,

@@ -495,6 +495,7 @@ __device__ __forceinline__ void pdl_trigger() {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 bool pdl_enabled();
+void set_pdl(int on);
 // fork a per-thread side stream off st (it waits for st's work so far) / join it back
 int side_fork(cudaStream_t st, cudaStream_t* side, cudaEvent_t* join);
 int side_join(cudaStream_t st, cudaStream_t side, cudaEvent_t join);

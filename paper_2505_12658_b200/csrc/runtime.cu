@@ -22,13 +22,17 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 // 6.95 s, tools/profile_serving.py --requests 400 --rate 90): early-launched dependents sit
 // on SMs the other stream could use.  The kernels keep their griddepcontrol points (no-ops
 // without the launch attribute).
+// Programmatic dependent launch: HY_PDL=1 / 0 forces it for the whole process; otherwise
+// the calling host thread's setting (hy_set_pdl), off by default.
+static thread_local int t_pdl = 0;
 bool pdl_enabled() {
-  static const bool on = [] {
+  static const int env = [] {
     const char* e = getenv("HY_PDL");
-    return e && e[0] == '1';
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  return on;
+  return env >= 0 ? env == 1 : t_pdl == 1;
 }
+void set_pdl(int on) { t_pdl = on ? 1 : 0; }
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 const char* get_last_error() { return g_last_error.c_str(); }
@@ -144,6 +148,10 @@ int make_tmap_3d_bf16(CUtensorMap* tm, const void* base, uint64_t d0, uint64_t d
 
 extern "C" const char* hy_last_error(void) { return hy::get_last_error(); }
 extern "C" int hy_version(void) { return 1; }
+extern "C" int hy_set_pdl(int on) {
+  hy::set_pdl(on);
+  return 0;
+}
 extern "C" int hy_device_sm_count(void) { return hy::num_sms(); }
 extern "C" long long hy_launch_count(void) { return hy::g_launches.load(); }
 
