@@ -7,8 +7,9 @@ Covers the paths with intra-kernel synchronisation worth checking: the GEMM's st
 last-arriver fixup (single-CTA normal and swap orientation, and the CTA-pair kernel with
 stream-K forced on), the pair kernel's cluster barriers, the tcgen05 attention kernels
 (paged prefill, varlen d = 64 / 80 / 128, one and two query tiles), decode attention (MHA
-split-KV + combine, GQA tensor-core), norms, RoPE append, argmax and the token-exact block
-copy.  Every result is checked against torch so a sanitizer-clean run is also a correct one.
+split-KV + combine, GQA tensor-core, the bulk-copy ticket kernel K8b and the co-resident
+tensor-core kernel K8c with its per-SM flags), the SLIM pair GEMM, GEMMs launched under
+programmatic dependent launch, norms, RoPE append, argmax and the token-exact block copy.  Every result is checked against torch so a sanitizer-clean run is also a correct one.
 """
 
 import math
@@ -99,7 +100,7 @@ def paged(n_heads, n_kv, chunks, tiles):
     os.environ.pop("HY_ATTN_T", None)
 
 
-def decode(n_heads, n_kv, ctxs):
+def decode(n_heads, n_kv, ctxs, kernel=None, co=False):
     """paged decode attention (split-KV + combine for long contexts; GQA tensor-core path
     for 4 <= group <= 16) over one layer of a 2-layer paged cache."""
     d, L, blk = 128, 2, 16
@@ -114,13 +115,18 @@ def decode(n_heads, n_kv, ctxs):
     ctx = torch.tensor(ctxs, dtype=torch.int32, device=DEV)
     wsb = lib.hy_attn_decode_workspace_bytes(n, n_heads, d, max(ctxs))
     ws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=DEV)
+    if kernel:
+        ck(lib.hy_set_decode_kernel(*kernel), "decode kernel")
+    lib.hy_set_decode_coresident(1 if co else 0)
     ck(lib.hy_attn_decode_paged(q.data_ptr(), n_heads * d, n, n_heads, n_kv, d,
                                 slots.data_ptr(), ctx.data_ptr(), max(ctxs), bt.data_ptr(), bts,
                                 kv.data_ptr() + 2 * n_kv * blk * d * 2, L * 2 * n_kv * blk * d,
                                 1 / math.sqrt(d), out.data_ptr(), n_heads * d, ws.data_ptr(),
                                 ws.numel(), st()), "decode")
     torch.cuda.synchronize()
-    print(f"decode heads {n_heads}/{n_kv} ctxs {ctxs}: ok", flush=True)
+    lib.hy_set_decode_kernel(0, 0)
+    lib.hy_set_decode_coresident(0)
+    print(f"decode heads {n_heads}/{n_kv} ctxs {ctxs} kernel {kernel} co {co}: ok", flush=True)
 
 
 def copy_tail():
@@ -142,6 +148,11 @@ def main():
     gemm(1100, 4096, 4096, {})
     gemm(1100, 2048, 4096, {"HY_PAIR_SK": "1", "HY_GEMM_MODE": "3"})
     gemm(577, 3072, 1024, {})
+    gemm(1100, 4096, 4096, {"HY_GEMM_SLIM": "1", "HY_GEMM_NOTABLE": "1"})
+    lib.hy_set_pdl(1)  # prologues overlapping the previous kernel (griddepcontrol)
+    gemm(16, 4096, 4096, {})
+    gemm(1100, 4096, 4096, {"HY_PAIR_SK": "1", "HY_GEMM_MODE": "3"})
+    lib.hy_set_pdl(0)
     for tiles in (1, 2):
         varlen(64, [577, 33], tiles)
         varlen(80, [300, 5], tiles)
@@ -150,6 +161,10 @@ def main():
         paged(28, 4, [(64, 16)], tiles)
     decode(32, 32, [616, 3000])
     decode(28, 4, [5, 900])
+    decode(8, 8, [616, 3000, 17], kernel=(2, 2))
+    decode(8, 8, [616, 3000, 17], kernel=(8, 3))
+    decode(32, 32, [616, 3000], co=True)
+    decode(28, 4, [5, 900], co=True)
     copy_tail()
     print("sanitize run complete")
 
