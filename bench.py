@@ -65,9 +65,11 @@ def parse():
     ap.add_argument("--devices", default=None,
                     help="comma list of CUDA device indices, one per GPU slot (default "
                          "0..N-1); repeating an index co-locates instances (functional tests)")
-    # >= ~40 s of arrivals at the goodput rate, so a burst cannot drain inside the 4 s TTFT
-    # bound and pass a rate the GPU cannot sustain (finite-trace artifact)
-    ap.add_argument("--requests", type=int, default=1500, help="trace requests per GPU")
+    # >= 30 s of arrivals at the goodput rate, so a burst cannot drain inside the
+    # 4 s TTFT bound and pass a rate the GPU cannot sustain (finite-trace artifact, BASELINE.md
+    # 2): 2,400 requests = 34 s at 71 req/s (1,500 gave 18 s at 84 req/s, with the device busy
+    # 24 s -- a backlog the 4 s TTFT allowance absorbed)
+    ap.add_argument("--requests", type=int, default=2400, help="trace requests per GPU")
     ap.add_argument("--rate-lo", type=float, default=16.0, help="per-GPU req/s")
     ap.add_argument("--rate-hi", type=float, default=128.0, help="per-GPU req/s")
     ap.add_argument("--no-e2e", action="store_true")
