@@ -300,18 +300,23 @@ __global__ void __launch_bounds__(64 + 256, 1)
       // per tile t the chain S_t(j) -> softmax_t(j) -> PV_t(j) -> S_t(j+1) is serial (P_t
       // lives in S_t's columns); the two tiles interleave so one tile's MMAs run while the
       // other tile's softmax works.  MMAs from this thread execute in issue order.
+      // a head dim narrower than the tile (DV = 80 in D = 128 tiles): Q K^T runs only the
+      // ceil(DV / 16) k-steps that hold real dims and P V only N = DV_16 output columns -- the
+      // zero-filled padding costs no MMA work (37.5% of both for Qwen2-VL's vision tower)
+      constexpr int KSTEPS = (DV + 15) / 16;
+      constexpr int DV16 = KSTEPS * 16;
       constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128);
-      constexpr uint32_t idesc_pv = idesc_bf16_f32(128, D) | (1u << 16);  // B (= V) MN-major
+      constexpr uint32_t idesc_pv = idesc_bf16_f32(128, DV16) | (1u << 16);  // B (= V) MN-major
       auto issue_s = [&](int t, int j) {
         const uint32_t q_addr = smem_u32(sQ + t * C::Q_BYTES);
         const uint32_t k_addr = smem_u32(sKV + (j & 1) * C::STAGE_BYTES);
 #pragma unroll
-        for (int c = 0; c < C::NC; ++c)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(tmem + t * 128, smem_desc_k_sw128(q_addr + c * C::CHUNK + k * 32),
-                      smem_desc_k_sw128(k_addr + c * C::CHUNK + k * 32), idesc_qk,
-                      (c | k) ? 1u : 0u);
+        for (int ks = 0; ks < KSTEPS; ++ks) {
+          const int c = ks >> 2, k = ks & 3;
+          umma_bf16(tmem + t * 128, smem_desc_k_sw128(q_addr + c * C::CHUNK + k * 32),
+                    smem_desc_k_sw128(k_addr + c * C::CHUNK + k * 32), idesc_qk,
+                    ks ? 1u : 0u);
+        }
         umma_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int j) {
@@ -359,12 +364,12 @@ __global__ void __launch_bounds__(64 + 256, 1)
         auto issue_s1 = [&](int j) {
           const uint32_t k_addr = smem_u32(sKV + (j & 1) * C::STAGE_BYTES);
 #pragma unroll
-          for (int c = 0; c < C::NC; ++c)
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              umma_bf16(tmem + (j & 1) * 128, smem_desc_k_sw128(q_addr + c * C::CHUNK + k * 32),
-                        smem_desc_k_sw128(k_addr + c * C::CHUNK + k * 32), idesc_qk,
-                        (c | k) ? 1u : 0u);
+          for (int ks = 0; ks < KSTEPS; ++ks) {
+            const int c = ks >> 2, k = ks & 3;
+            umma_bf16(tmem + (j & 1) * 128, smem_desc_k_sw128(q_addr + c * C::CHUNK + k * 32),
+                      smem_desc_k_sw128(k_addr + c * C::CHUNK + k * 32), idesc_qk,
+                      ks ? 1u : 0u);
+          }
           umma_commit(&s_full[j & 1]);
           umma_commit(&k_empty[j & 1]);
         };
@@ -665,15 +670,22 @@ static int launch_tc_attn(const CUtensorMap& tq, const CUtensorMap& tkv, const T
   return 0;
 }
 
-// Query tiles per CTA.  Two (ping-pong between the tiles) measured fastest except when the
-// grid would not cover half the SMs (a single small image: 48 CTAs), where one tile per CTA
-// with two softmax threads per row doubles the CTAs (1-image ViT 15.5 -> 9.7 us; 2304-token
-// prefill 91 us with two tiles, 118 with one).  HY_ATTN_T=1/2 forces.
+// Query tiles per CTA: two (ping-pong between the tiles) or one (two softmax threads per
+// row, twice the CTAs), whichever the wave count favours.  HY_ATTN_T=1/2 forces.
 static int attn_tiles(int n_seqs, int max_q, int n_heads) {
   const char* e = getenv("HY_ATTN_T");
   const int forced = e ? atoi(e) : 0;
   if (forced == 1 || forced == 2) return forced;
-  return (long long)n_seqs * ceil_div(max_q, 256) * n_heads < 64 ? 1 : 2;
+  // waves of CTAs x the CTA's time: a two-tile CTA takes ~1.6x a one-tile CTA (its
+  // ping-pong makes each tile ~20% cheaper).  Matches every measured case (ViT 1-32 images
+  // of 577 / 576-11664 tokens, prefill chunks 616-2304): e.g. one 2916-token Qwen2-VL image
+  // 192 two-tile CTAs (2 waves) 117 us vs 368 one-tile CTAs (3 waves) 91 us
+  const long long sms = num_sms();
+  const long long c2 = (long long)n_seqs * ceil_div(max_q, 256) * n_heads;
+  const long long c1 = (long long)n_seqs * ceil_div(max_q, 128) * n_heads;
+  const double t2 = 1.6 * (double)((c2 + sms - 1) / sms);
+  const double t1 = (double)((c1 + sms - 1) / sms);
+  return t1 < t2 ? 1 : 2;
 }
 
 // Paged prefill: Q rows of the chunk batch [n_rows, ld_q]; K/V from the paged cache of one

@@ -145,8 +145,11 @@ def attn_sweep(out):
         flash_attn_varlen_func = None
     # ViT: n images x T tokens: LLaVA 16 heads x 64 (577 tokens), Qwen2-VL 16 heads x 80
     # (dynamic resolution)
-    for n_img, T, d in ((1, 577, 64), (3, 577, 64), (8, 577, 64), (32, 577, 64), (1, 2916, 80),
-                        (4, 1024, 80), (8, 576, 80)):
+    vit = ((1, 577, 64), (3, 577, 64), (8, 577, 64), (32, 577, 64), (1, 2916, 80),
+           (4, 1024, 80), (8, 576, 80))
+    if os.environ.get("ATTN_VIT_SHAPES"):  # "images/tokens/head_dim;..."
+        vit = [tuple(int(v) for v in x.split("/")) for x in os.environ["ATTN_VIT_SHAPES"].split(";")]
+    for n_img, T, d in vit:
         nh = 16
         tot = n_img * T
         qkv = torch.randn(tot, 3 * nh * d, device=DEV).bfloat16()
