@@ -742,6 +742,213 @@ __global__ void __launch_bounds__(64 + 32 * kEpiWarps, 1)
 }
 
 // ---------------------------------------------------------------------------
+// K1c: swap-AB decode GEMM split over K inside a thread-block cluster.  The KS CTAs of a
+// cluster share one 128-row weight tile, rank r reducing k-blocks [r nkb / KS, (r+1) nkb / KS)
+// -- so a decode GEMM with few weight tiles (N = 4096: 32 tiles) still streams its weights
+// through ~all SMs -- and the partial sums meet in DISTRIBUTED shared memory: ranks 1..KS-1
+// store their fp32 accumulators into rank 0's reduction buffer (st.shared::cluster), one
+// cluster barrier (release / acquire), and rank 0 adds them in rank order (deterministic)
+// and runs the swap epilogue.  This replaces stream-K's global partials, fences and arrival
+// atomics (a 3-4 us tail) with one DSMEM round trip.
+// ---------------------------------------------------------------------------
+template <int BN>
+struct CskCfg {
+  static constexpr int BK = 64;
+  static constexpr int A_BYTES = 128 * BK * 2;  // weight rows (MMA-M)
+  static constexpr int B_BYTES = BN * BK * 2;   // token rows (MMA-N)
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int RED_SLOT = 128 * BN * 4;  // one rank's fp32 accumulator
+  static constexpr int EPI_WARPS = 4;
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  static int smem_bytes(int stages, int ks) {
+    return stages * STAGE_BYTES + (ks - 1) * RED_SLOT + EPI_WARPS * kStgBytes + 1024 + 256;
+  }
+};
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(64 + 32 * 4, 1)
+    gemm_swap_csk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                         const GemmArgs a, int stages, int ks) {
+  using C = CskCfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + stages * C::A_BYTES;
+  uint8_t* red = sB + stages * C::B_BYTES;  // [ks - 1][BN / 32][8][128] float4 (rank 0 only)
+  uint8_t* stg = red + (ks - 1) * C::RED_SLOT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + C::EPI_WARPS * kStgBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + stages;
+  uint64_t* tfull = bars + 2 * stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int p = blockIdx.x / ks;  // weight tile
+  const int kb0 = (int)((long long)rank * a.nkb / ks), kb1 = (int)((long long)(rank + 1) * a.nkb / ks);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();  // after the TMEM allocation (see gemm_tc_kernel)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // weights of the first stages before the grid dependency resolves; the activations
+      // too when launched without PDL
+      int npre = 0;
+      for (int kb = kb0; kb < kb1 && npre < stages; ++kb, ++npre) {
+        mbar_expect_tx(&full[npre], C::STAGE_BYTES);
+        tma_load_2d(&tmW, &full[npre], sA + npre * C::A_BYTES, kb * C::BK, p * 128, kEvictFirst);
+        if (a.dbg & 16)
+          tma_load_2d(&tmX, &full[npre], sB + npre * C::B_BYTES, kb * C::BK, 0, kEvictLast);
+      }
+      pdl_wait();
+      int stage = 0;
+      uint32_t phase = 0;
+      int g = 0;
+      for (int kb = kb0; kb < kb1; ++kb, ++g) {
+        if (g < npre) {
+          if (!(a.dbg & 16))
+            tma_load_2d(&tmX, &full[stage], sB + stage * C::B_BYTES, kb * C::BK, 0, kEvictLast);
+        } else {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(&tmW, &full[stage], sA + stage * C::A_BYTES, kb * C::BK, p * 128, kEvictFirst);
+          tma_load_2d(&tmX, &full[stage], sB + stage * C::B_BYTES, kb * C::BK, 0, kEvictLast);
+        }
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(sA + stage * C::A_BYTES);
+        const uint32_t b_addr = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < C::BK / 16; ++k)
+          umma_bf16(tmem_base, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32),
+                    idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+        umma_commit(&empty[stage]);
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      umma_commit(tfull);
+    }
+  } else if (rank != 0) {
+    // ---- ranks 1..ks-1: accumulators into rank 0's reduction buffer (lane-coalesced float4)
+    const int sub = warp & 3;
+    const int lrow = sub * 32 + lane;
+    mbar_wait_sleepy(tfull, 0);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + ((uint32_t)(sub * 32) << 16);
+    const uint32_t dst = mapa_shared(smem_u32(red + (rank - 1) * C::RED_SLOT), 0);
+#pragma unroll
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(taddr + c * 32, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                         dst + (uint32_t)(((c * 8 + j / 4) * 128 + lrow) * 16)),
+                     "r"(r[j]), "r"(r[j + 1]), "r"(r[j + 2]), "r"(r[j + 3])
+                     : "memory");
+    }
+  }
+  // every thread of every CTA: the remote stores are visible to rank 0 past this barrier
+  tc_fence_before();
+  cluster_sync();
+  if (rank == 0 && warp >= 2) {
+    // ---- rank 0: own accumulators + the others' in rank order, then the swap epilogue
+    const int sub = warp & 3;
+    const int lrow = sub * 32 + lane;
+    mbar_wait_sleepy(tfull, 0);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + ((uint32_t)(sub * 32) << 16);
+    int nst = 0;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(taddr + c * 32, r);
+      tmem_ld_wait();
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      for (int q = 0; q < ks - 1; ++q) {
+        const uint32_t src = smem_u32(red + q * C::RED_SLOT);
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 f = lds_f32x4(src + (uint32_t)(((c * 8 + j / 4) * 128 + lrow) * 16));
+          v[j] += f.x;
+          v[j + 1] += f.y;
+          v[j + 2] += f.z;
+          v[j + 3] += f.w;
+        }
+      }
+      epi_chunk<EPI, true>(a, p * 128 + sub * 32, c * 32, v, lane,
+                           smem_u32(stg) + (warp - 2) * kStgBytes, nullptr, nst);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+template <int BN, int EPI>
+static int launch_csk(const CUtensorMap& tW, const CUtensorMap& tX, const GemmArgs& a, int tiles,
+                      int ks, int stages, cudaStream_t st) {
+  using C = CskCfg<BN>;
+  const int smem = C::smem_bytes(stages, ks);
+  auto kern = gemm_swap_csk_kernel<BN, EPI>;
+  HY_CUDA_RET(ensure_smem(kern, 227 * 1024));
+  HY_CUDA_RET(ensure_max_carveout(kern));
+  HY_CUDA_RET(launch_pdl_cluster(kern, dim3(tiles * ks), dim3(C::THREADS), (size_t)smem, ks, st,
+                                 tW, tX, a, stages, ks));
+  HY_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int BN>
+static int launch_csk_epi(int epi, const CUtensorMap& tW, const CUtensorMap& tX, const GemmArgs& a,
+                          int tiles, int ks, int stages, cudaStream_t st) {
+  switch (epi) {
+    case EPI_BF16: return launch_csk<BN, EPI_BF16>(tW, tX, a, tiles, ks, stages, st);
+    case EPI_QGELU: return launch_csk<BN, EPI_QGELU>(tW, tX, a, tiles, ks, stages, st);
+    case EPI_GELU: return launch_csk<BN, EPI_GELU>(tW, tX, a, tiles, ks, stages, st);
+    case EPI_SWIGLU: return launch_csk<BN, EPI_SWIGLU>(tW, tX, a, tiles, ks, stages, st);
+    case EPI_F32: return launch_csk<BN, EPI_F32>(tW, tX, a, tiles, ks, stages, st);
+    default: return -1;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1b: CTA-pair GEMM (tcgen05.mma.cta_group::2), normal orientation, pair tile 256 x BN.
 //
 // The two CTAs of a cluster sit on the two SMs of one TPC.  Each loads its own 128 token
@@ -1355,6 +1562,37 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   a.nkb = ceil_div(K, 64);
   const int T = a.np * a.nq;
   const int sms = gemm_sms();
+  // decode GEMMs with few weight tiles (M <= 64, 128-row weight tiles * 2 <= SMs): split K
+  // inside a cluster, reduced through distributed shared memory (K1c) -- HY_GEMM_NOCSK=1 off
+  const char* csk_env = getenv("HY_GEMM_CSK");  // tuning: cluster size (any weight-tile count)
+  if (swap && M <= 64 && (2 * a.np <= sms || csk_env) && !getenv("HY_GEMM_NOCSK") &&
+      !(a.dbg & 2)) {
+    const int cbn = M <= 32 ? 32 : 64;
+    int ks = std::min(8, sms / a.np);
+    while (ks > 1 && a.nkb / ks < 4) --ks;
+    if (csk_env) ks = std::max(1, std::min(8, atoi(csk_env)));
+    if (ks >= 2) {
+      const int red = (ks - 1) * (cbn == 32 ? CskCfg<32>::RED_SLOT : CskCfg<64>::RED_SLOT);
+      const int stage = cbn == 32 ? CskCfg<32>::STAGE_BYTES : CskCfg<64>::STAGE_BYTES;
+      const int budget = 227 * 1024 - red - 4 * kStgBytes - 1024 - 256;
+      int stages = std::min(8, budget / stage);
+      if (const char* e = getenv("HY_GEMM_CSK_STAGES")) stages = std::min(stages, atoi(e));  // tuning
+      if (stages >= 2) {
+        a.nq = 1;
+        if (!pdl_enabled()) a.dbg |= 16;
+        CUtensorMap tW, tX;
+        HY_RET_IF(make_tmap_2d_bf16(&tW, W, N, K, (uint64_t)ldw * 2, 128, 64));
+        HY_RET_IF(make_tmap_2d_bf16(&tX, A, M, K, (uint64_t)lda * 2, cbn, 64));
+        const int rc = cbn == 32 ? launch_csk_epi<32>(epi, tW, tX, a, a.np, ks, stages, st)
+                                 : launch_csk_epi<64>(epi, tW, tX, a, a.np, ks, stages, st);
+        if (rc < 0) {
+          set_last_error("gemm: no cluster split-K kernel for this epilogue");
+          return (int)cudaErrorInvalidValue;
+        }
+        return rc;
+      }
+    }
+  }
   const size_t need = kCounterBytes + (size_t)sms * 2 * 128 * bn * sizeof(float);
   // stream-K when whole-tile waves would leave SMs idle.  Swap orientation (decode: weight
   // streaming, every SM must pull bytes): a mostly idle last wave (fill < 85%) or a single

@@ -63,7 +63,12 @@ def _gemm_ref(A, W, bias, act, res):
 
 
 @pytest.mark.parametrize("M,N,K,mode,act,bias,res,f32", [
-    (1, 4096, 4096, 0, 0, False, False, False),      # decode: swap-AB + split-K
+    (1, 4096, 4096, 0, 0, False, False, False),      # decode: swap-AB, cluster split-K (K1c)
+    (16, 4096, 4096, 0, 0, False, True, False),      # K1c: o-proj + in-place residual, 4 ranks
+    (48, 3584, 3584, 0, 0, True, False, False),      # K1c: Qwen2-VL o shape, 5 ranks, BN 64
+    (64, 4096, 11008, 0, 0, False, True, False),     # K1c: down-proj + residual
+    (32, 4608, 3584, 0, 0, True, False, False),      # K1c: Qwen2-VL qkv (bias), 4 ranks
+    (9, 4096, 512, 0, 1, True, False, False),        # K1c: short K (2 ranks), QuickGELU
     (7, 12288, 512, 0, 0, False, True, False),
     (33, 1536, 512, 0, 4, False, False, False),       # swap-AB + SwiGLU (shuffle pairing)
     (64, 2816, 512, 1, 4, False, False, False),
