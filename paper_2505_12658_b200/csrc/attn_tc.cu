@@ -121,7 +121,9 @@ struct TcAttnCfg {
   // T = 2: two query tiles per CTA, 4 softmax warps each, ping-pong between the tiles.
   // T = 1: one query tile, 8 softmax warps (two threads per row, 64 keys each), S double-
   //        buffered over key tiles so Q K^T of tile j+1 runs under the softmax of tile j.
-  static constexpr int TILES = T;
+  // T = 3: two query tiles ping-ponging like T = 2, each with 8 softmax warps (two threads per
+  //        row like T = 1): half the per-thread softmax chain, 16 softmax warps per CTA.
+  static constexpr int TILES = T == 3 ? 2 : T;
   static constexpr int NC = D / 64;               // 64-wide d chunks (one 128B swizzle row)
   static constexpr int CHUNK = 128 * 128;         // bytes of one [128 rows][64 bf16] chunk
   static constexpr int Q_BYTES = NC * CHUNK;      // one query tile
@@ -131,14 +133,14 @@ struct TcAttnCfg {
   // TMEM columns: tile t owns S_t (fp32, 128 cols) at t * 128, overwritten in place by P_t
   // (bf16 pairs, first 64 cols), and O_t at 256 + t * 128
   static constexpr int TMEM_COLS = 512;
-  static constexpr int THREADS = 64 + 256;
+  static constexpr int THREADS = T == 3 ? 64 + 512 : 64 + 256;
 };
 
 // DV: the real head dim when it is narrower than the D-wide tiles (varlen only): Q/K/V are
 // fetched through a 3D map [rows][heads][DV] whose boxes past DV are zero-filled, so the
 // padded dims add nothing to S and leave O's extra columns zero; only DV columns are stored.
 template <int D, bool PAGED, int T, int DV = D>
-__global__ void __launch_bounds__(64 + 256, 1)
+__global__ void __launch_bounds__(T == 3 ? 64 + 512 : 64 + 256, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                    const TcAttnParams p) {
   using C = TcAttnCfg<D, T>;
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(64 + 256, 1)
   // the pair's second tile holds no query row (a sequence's last, partial pair): it is
   // skipped -- no Q K^T / P V issued, its softmax warps idle (e.g. a 577-token image: 5 of
   // 6 tiles computed instead of 6)
-  const bool t1_live = T == 2 && qbase + C::BQ < nq;
+  const bool t1_live = C::TILES == 2 && qbase + C::BQ < nq;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(64 + 256, 1)
       mbar_wait(q_full, 0);
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
-      if constexpr (T == 2) {
+      if constexpr (C::TILES == 2) {
       issue_s(0, 0);
       if (t1_live) issue_s(1, 0);
       umma_commit(&k_empty[0]);  // K_0 retired once both Q K^T complete
@@ -522,30 +524,37 @@ __global__ void __launch_bounds__(64 + 256, 1)
     }
 
     } else {
-    // ---------------- softmax, one query tile: warps 2..9, two threads per row --------------
-    // warp w and w + 4 own the same 32 TMEM lanes (rows); the first takes keys [0, 64) of
-    // each key tile, the second [64, 128).  Row maxima are exchanged through shared memory
-    // (double-buffered by tile parity) with a 64-thread named barrier per row group.
-    __shared__ float xm[2][2][128];  // [tile parity][key half][row]
-    __shared__ float xl[2][128];
+    // ---------------- softmax, two threads per row ------------------------------------------
+    // T = 1: one query tile, warps 2..9.  T = 3: two tiles, warps 2..9 (tile 0) and 10..17
+    // (tile 1).  Warps w and w + 4 of a tile own the same 32 TMEM lanes (rows); the first
+    // takes keys [0, 64) of each key tile, the second [64, 128).  Row maxima are exchanged
+    // through shared memory (double-buffered by key-tile parity) with a 64-thread named
+    // barrier per (tile, row group).  T = 1 double-buffers S over key tiles (buffer j & 1);
+    // T = 3 keeps S_t in buffer t, ping-ponging with the other tile like T = 2.
+    __shared__ float xm[2][2][2][128];  // [tile][key-tile parity][key half][row]
+    __shared__ float xl[2][2][128];     // [tile][key half][row]
+    const int t = T == 3 ? (warp - 2) >> 3 : 0;
     const int sub = warp & 3;
-    const int hc = (warp - 2) >> 2;  // key / O-column half
+    const int hc = ((warp - 2) >> 2) & 1;  // key / O-column half
     const int row = sub * 32 + lane;
+    const int bar_id = 1 + t * 4 + sub;
     const uint32_t tl = tmem + ((uint32_t)(sub * 32) << 16);
-    const uint32_t tO = tl + 256 + hc * (D / 2);
-    const int qrow = qbase + row;
+    const uint32_t tO = tl + 256 + t * 128 + hc * (D / 2);
+    const int qrow = qbase + t * C::BQ + row;
     const int qpos = off + qrow;
     const int kmax = PAGED ? min(kv_len, qpos + 1) : kv_len;  // keys [0, kmax) are valid
+    const bool live = t == 0 || t1_live;
     float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kt; ++j) {
+    for (int j = 0; j < (live ? n_kt : 0); ++j) {
       const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+      const int sb = T == 3 ? t : b;  // S / P buffer
+      mbar_wait(&s_full[sb], T == 3 ? (j & 1) : ((j >> 1) & 1));
       tc_fence_after();
       const int kbase = j * C::BK + hc * 64;
       const bool full = __all_sync(0xffffffffu, kbase + 64 <= kmax);
       uint32_t r[64];
-      tmem_ld_32x32b_x32(tl + b * 128 + hc * 64, r);
-      tmem_ld_32x32b_x32(tl + b * 128 + hc * 64 + 32, r + 32);
+      tmem_ld_32x32b_x32(tl + sb * 128 + hc * 64, r);
+      tmem_ld_32x32b_x32(tl + sb * 128 + hc * 64 + 32, r + 32);
       tmem_ld_wait();
       float mx8[8];
 #pragma unroll
@@ -560,13 +569,13 @@ __global__ void __launch_bounds__(64 + 256, 1)
       }
       float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      xm[b][hc][row] = mx;
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + sub) : "memory");
-      mx = fmaxf(mx, xm[b][hc ^ 1][row]);
+      xm[t][b][hc][row] = mx;
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      mx = fmaxf(mx, xm[t][b][hc ^ 1][row]);
       mx = mx == -INFINITY ? mx : mx * p.scale_log2;
       const float m_new = fmaxf(m_used, mx);
       if (j >= 1) {
-        mbar_wait(&o_done[0], (j - 1) & 1);  // P V(j-1) retired: O stable
+        mbar_wait(&o_done[t], (j - 1) & 1);  // P V(j-1) retired: O stable
         tc_fence_after();
         const bool need = m_new > m_used + 8.f;
         if (__any_sync(0xffffffffu, need)) {
@@ -611,7 +620,7 @@ __global__ void __launch_bounds__(64 + 256, 1)
           rs2[u & 1] = fadd2(rs2[u & 1], pk2(e0, e1));
           pk[u] = pack_bf16x2(e0, e1);
         }
-        tmem_st_32x32b_x16(tl + b * 128 + hc * 32 + c * 16, pk);
+        tmem_st_32x32b_x16(tl + sb * 128 + hc * 32 + c * 16, pk);
       }
       float ra, rb, rc, rd;
       up2(rs2[0], ra, rb);
@@ -620,13 +629,14 @@ __global__ void __launch_bounds__(64 + 256, 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[0]);
+      if (lane == 0) mbar_arrive(&p_full[t]);
     }
     // O / (l_lo + l_hi) -> global, each thread its half of the head dims
-    xl[hc][row] = l;
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + sub) : "memory");
-    const float lt = l + xl[hc ^ 1][row];
-    mbar_wait(&o_done[0], (n_kt - 1) & 1);
+    if (live) {
+    xl[t][hc][row] = l;
+    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+    const float lt = l + xl[t][hc ^ 1][row];
+    mbar_wait(&o_done[t], (n_kt - 1) & 1);
     tc_fence_after();
     const float inv = lt > 0.f ? 1.f / lt : 0.f;
 #pragma unroll 1
@@ -646,6 +656,7 @@ __global__ void __launch_bounds__(64 + 256, 1)
           store_bf16x8(dst + u, v);
         }
       }
+    }
     }
     }
   }
@@ -675,7 +686,7 @@ static int launch_tc_attn(const CUtensorMap& tq, const CUtensorMap& tkv, const T
 static int attn_tiles(int n_seqs, int max_q, int n_heads) {
   const char* e = getenv("HY_ATTN_T");
   const int forced = e ? atoi(e) : 0;
-  if (forced == 1 || forced == 2) return forced;
+  if (forced >= 1 && forced <= 3) return forced;
   // waves of CTAs x the CTA's time: a two-tile CTA takes ~1.6x a one-tile CTA (its
   // ping-pong makes each tile ~20% cheaper).  Matches every measured case (ViT 1-32 images
   // of 577 / 576-11664 tokens, prefill chunks 616-2304): e.g. one 2916-token Qwen2-VL image
@@ -703,7 +714,7 @@ int attn_tc_prefill(const void* q, int ld_q, int n_rows, int n_seqs, const int* 
   p.block_table = block_table;
   p.bt_stride = bt_stride;
   const int T = attn_tiles(n_seqs, max_q, n_heads);
-  p.q_tiles = ceil_div(max_q, 128 * T);
+  p.q_tiles = ceil_div(max_q, 128 * (T == 3 ? 2 : T));
   p.group = n_heads / n_kv_heads;
   p.rows_per_block = block_stride / head_dim;
   p.rows_per_kv = n_kv_heads * HY_KV_BLOCK_TOKENS;
@@ -719,6 +730,9 @@ int attn_tc_prefill(const void* q, int ld_q, int n_rows, int n_seqs, const int* 
   if (T == 2)
     return head_dim == 128 ? launch_tc_attn<128, true, 2>(tq, tkv, p, n_seqs, n_heads, st)
                            : launch_tc_attn<64, true, 2>(tq, tkv, p, n_seqs, n_heads, st);
+  if (T == 3)
+    return head_dim == 128 ? launch_tc_attn<128, true, 3>(tq, tkv, p, n_seqs, n_heads, st)
+                           : launch_tc_attn<64, true, 3>(tq, tkv, p, n_seqs, n_heads, st);
   return head_dim == 128 ? launch_tc_attn<128, true, 1>(tq, tkv, p, n_seqs, n_heads, st)
                          : launch_tc_attn<64, true, 1>(tq, tkv, p, n_seqs, n_heads, st);
 }
@@ -732,7 +746,7 @@ int attn_tc_varlen(const void* qkv, int ld_qkv, int n_rows, int n_segs, const in
   TcAttnParams p{};
   p.qstart = seg;
   const int T = attn_tiles(n_segs, max_len, n_heads);
-  p.q_tiles = ceil_div(max_len, 128 * T);
+  p.q_tiles = ceil_div(max_len, 128 * (T == 3 ? 2 : T));
   p.group = 1;
   p.k_col0 = n_heads * head_dim;
   p.v_col0 = 2 * n_heads * head_dim;
@@ -748,14 +762,18 @@ int attn_tc_varlen(const void* qkv, int ld_qkv, int n_rows, int n_segs, const in
     p.v_col0 = 2 * n_heads;
     HY_RET_IF(make_tmap_3d_bf16(&tm, qkv, 80, (uint64_t)3 * n_heads, n_rows, 80 * 2,
                                 (uint64_t)ld_qkv * 2, 64, 128));
-    return T == 2 ? launch_tc_attn<128, false, 2, 80>(tm, tm, p, n_segs, n_heads, st)
-                  : launch_tc_attn<128, false, 1, 80>(tm, tm, p, n_segs, n_heads, st);
+    return T == 2   ? launch_tc_attn<128, false, 2, 80>(tm, tm, p, n_segs, n_heads, st)
+           : T == 3 ? launch_tc_attn<128, false, 3, 80>(tm, tm, p, n_segs, n_heads, st)
+                    : launch_tc_attn<128, false, 1, 80>(tm, tm, p, n_segs, n_heads, st);
   }
   HY_RET_IF(make_tmap_2d_bf16(&tm, qkv, n_rows, (uint64_t)3 * n_heads * head_dim,
                               (uint64_t)ld_qkv * 2, 128, 64));
   if (T == 2)
     return head_dim == 128 ? launch_tc_attn<128, false, 2>(tm, tm, p, n_segs, n_heads, st)
                            : launch_tc_attn<64, false, 2>(tm, tm, p, n_segs, n_heads, st);
+  if (T == 3)
+    return head_dim == 128 ? launch_tc_attn<128, false, 3>(tm, tm, p, n_segs, n_heads, st)
+                           : launch_tc_attn<64, false, 3>(tm, tm, p, n_segs, n_heads, st);
   return head_dim == 128 ? launch_tc_attn<128, false, 1>(tm, tm, p, n_segs, n_heads, st)
                          : launch_tc_attn<64, false, 1>(tm, tm, p, n_segs, n_heads, st);
 }

@@ -47,7 +47,7 @@ KVB = MC.KV_BLOCK_TOKENS
 CLOCKS = ("oracle", "device", "wall")
 _BATCH_SEQ = itertools.count()  # global batch order, to merge tokens across instances
 # programmatic dependent launch per batch: "decode" (decode-only language batches without
-# vision work), "never", "always"
+# vision work), "novis" (any batch without vision work), "never", "always"
 _PDL_POLICY = os.environ.get("HY_PDL_POLICY", "decode")
 
 
@@ -404,7 +404,8 @@ class InstanceRuntime:
         # PDL for decode-only batches without vision work (hy_set_pdl; HY_PDL_POLICY=never
         # keeps it off, =always on for every batch)
         lib.hy_set_pdl(1 if _PDL_POLICY == "always" or (
-            _PDL_POLICY == "decode" and not batch.prefill_chunks and not has_vis) else 0)
+            _PDL_POLICY == "decode" and not batch.prefill_chunks and not has_vis) or (
+            _PDL_POLICY == "novis" and not has_vis) else 0)
         if sampler is not None:
             sampler.before_batch(solo=not (has_lang and has_vis))
         out_rids: List[str] = []
