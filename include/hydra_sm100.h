@@ -22,11 +22,13 @@
  *   - every pointer is device memory (or a mapped peer pointer) unless stated;
  *   - int32 metadata arrays are device resident; host arrays are marked "host";
  *   - any host thread may call with its own stream, on any device.  Process-wide state is
- *     limited to: the per-(device, kernel) shared-memory attribute cache (mutex guarded),
- *     one side stream + events per (host thread, device, priority), tuning knobs read once
- *     from the environment (HY_*; defaults are the measured best), the launch counter
- *     (hy_launch_count) and the optional kernel timer hook (hy_set_kernel_timer, a
- *     bench/test instrument that must not be set while several threads launch);
+ *     limited to: the per-(device, kernel) shared-memory attribute and carveout caches
+ *     (mutex guarded), one side stream + events per (host thread, device, priority), tuning
+ *     knobs read from the environment (HY_*; defaults are the measured best), the measured
+ *     GEMM dispatch table (constant, compiled in), the launch counter (hy_launch_count) and
+ *     the optional kernel timer hook (hy_set_kernel_timer, a bench/test instrument that must
+ *     not be set while several threads launch).  Per-host-thread settings: hy_set_pdl,
+ *     hy_set_decode_kernel, hy_set_decode_coresident;
  *   - nothing falls back to the CPU: a missing device or bad argument is an error.
  *
  * Paged layouts (one instance = one GPU)

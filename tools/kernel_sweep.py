@@ -289,12 +289,19 @@ def decode_sweep(out):
     shapes = ((32, 32, 256, 660, 0), (32, 32, 256, 660, 1), (32, 32, 128, 700, 1),
               (32, 32, 64, 700, 1), (32, 32, 32, 700, 1), (28, 4, 256, 660, 0),
               (28, 4, 64, 4000, 0), (32, 8, 256, 660, 0), (32, 32, 16, 8000, 0))
-    if os.environ.get("DECODE_SHAPES"):  # "nh/nkv/seqs/ctx/shuffled;..."
-        shapes = [tuple(int(v) for v in x.split("/")) for x in os.environ["DECODE_SHAPES"].split(";")]
+    if os.environ.get("DECODE_SHAPES"):  # "nh/nkv/seqs/ctx/shuffled;..." (ctx "lo-hi": random)
+        shapes = [tuple(v if "-" in v else int(v) for v in x.split("/"))
+                  for x in os.environ["DECODE_SHAPES"].split(";")]
     if os.environ.get("DECODE_CO"):
         lib().hy_set_decode_coresident(1)
     for nh, nkv, n, ctx, shuffled in shapes:
         d = 128
+        if isinstance(ctx, str):  # per-sequence contexts drawn from [lo, hi]
+            lo, hi = (int(v) for v in ctx.split("-"))
+            cl = torch.randint(lo, hi + 1, (n,), generator=torch.Generator().manual_seed(0))
+            ctx = int(cl.max())
+        else:
+            cl = torch.full((n,), ctx)
         nb = -(-ctx // 16)
         be = 2 * nkv * 16 * d
         kv = torch.randn(n * nb + 1, be, device=DEV).bfloat16()
@@ -304,7 +311,7 @@ def decode_sweep(out):
         q = torch.randn(n, nh * d, device=DEV).bfloat16()
         o = torch.empty_like(q)
         slots = torch.arange(n, dtype=torch.int32, device=DEV)
-        ctxs = torch.full((n,), ctx, dtype=torch.int32, device=DEV)
+        ctxs = cl.to(torch.int32).to(DEV)
         wsb = lib().hy_attn_decode_workspace_bytes(n, nh, d, ctx)
         ws = torch.zeros(max(wsb, 16), dtype=torch.uint8, device=DEV)
 
@@ -315,7 +322,7 @@ def decode_sweep(out):
                                             ws.data_ptr(), ws.numel(), st())
             assert rc == 0, lib().hy_last_error()
         t = timeit(ours)
-        byt = n * ctx * 2 * nkv * d * 2
+        byt = int(cl.sum()) * 2 * nkv * d * 2
         r = {"name": "decode_attn", "n_heads": nh, "n_kv": nkv, "seqs": n, "ctx": ctx,
              "shuffled_blocks": bool(shuffled), "us": t * 1e3, "gbs": byt / t / 1e6}
         out.append(r)
