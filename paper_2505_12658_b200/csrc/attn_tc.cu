@@ -139,8 +139,11 @@ struct TcAttnCfg {
 // DV: the real head dim when it is narrower than the D-wide tiles (varlen only): Q/K/V are
 // fetched through a 3D map [rows][heads][DV] whose boxes past DV are zero-filled, so the
 // padded dims add nothing to S and leave O's extra columns zero; only DV columns are stored.
+#ifndef HY_ATTN_MAXNREG
+#define HY_ATTN_MAXNREG 200
+#endif
 template <int D, bool PAGED, int T, int DV = D>
-__global__ void __launch_bounds__(T == 3 ? 64 + 512 : 64 + 256, 1)
+__global__ void __launch_bounds__(T == 3 ? 64 + 512 : 64 + 256, 1) __maxnreg__(T == 3 ? 112 : HY_ATTN_MAXNREG)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                    const TcAttnParams p) {
   using C = TcAttnCfg<D, T>;
@@ -418,20 +421,25 @@ __global__ void __launch_bounds__(T == 3 ? 64 + 512 : 64 + 256, 1)
       const int kbase = j * C::BK;
       const int kmax = PAGED ? min(kv_len, qpos + 1) : kv_len;  // keys [0, kmax) are valid
       const bool full = __all_sync(0xffffffffu, kbase + C::BK <= kmax);
-      uint32_t r[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tS + c * 32, r + c * 32);
-      tmem_ld_wait();
+      // The S row is read from TMEM twice, 64 columns at a time (max, then exp): holding all
+      // 128 fp32 values in registers spilled at the 168 registers a 10-warp CTA can have
+      uint32_t r[64];
       float mx8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
-      if (full) {
 #pragma unroll
-        for (int u = 0; u < 128; ++u) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
-      } else {
+      for (int hh = 0; hh < 2; ++hh) {
+        tmem_ld_32x32b_x32(tS + hh * 64, r);
+        tmem_ld_32x32b_x32(tS + hh * 64 + 32, r + 32);
+        tmem_ld_wait();
+        if (full) {
 #pragma unroll
-        for (int u = 0; u < 128; ++u)
-          if (kbase + u < kmax) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
+          for (int u = 0; u < 64; ++u) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
+        } else {
+#pragma unroll
+          for (int u = 0; u < 64; ++u)
+            if (kbase + hh * 64 + u < kmax) mx8[u & 7] = fmaxf(mx8[u & 7], __uint_as_float(r[u]));
+        }
       }
       float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
@@ -466,14 +474,22 @@ __global__ void __launch_bounds__(T == 3 ? 64 + 512 : 64 + 256, 1)
       // columns per store; column c of P holds keys 2c, 2c+1 (already in registers)
       uint64_t rs2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
       const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2), nms2 = pk2(-ms, -ms);
+      // second read, in order: P of chunk c goes to columns [16c, 16c + 16), which belong to S
+      // chunks <= c, already read
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
+        if ((c & 1) == 0) {
+          tmem_ld_32x32b_x32(tS + c * 32, r);
+          tmem_ld_32x32b_x32(tS + c * 32 + 32, r + 32);
+          tmem_ld_wait();
+        }
         uint32_t pk[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           const int k0 = c * 32 + 2 * u;
+          const int kr = (c & 1) * 32 + 2 * u;  // register index of key k0
           float x0, x1;
-          up2(ffma2(pk2(__uint_as_float(r[k0]), __uint_as_float(r[k0 + 1])), sc2, nms2), x0, x1);
+          up2(ffma2(pk2(__uint_as_float(r[kr]), __uint_as_float(r[kr + 1])), sc2, nms2), x0, x1);
           float e0, e1;
           if (u < HY_ATTN_POLY) {
             exp2_poly2(x0, x1, e0, e1);

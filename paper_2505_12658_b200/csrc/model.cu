@@ -318,6 +318,21 @@ extern "C" int hy_vit_forward(const HyVitModel* m, const HyVitBatch* b, void* wo
                ((long long)M << 42) | ((long long)N << 21) | (long long)K);
     return rc;
   };
+  // HY_VIT_SMS=<n> (A/B): the ViT's GEMM grids use at most n SMs, so a concurrent language
+  // batch keeps the rest (the vision stream is rarely the batch's critical path)
+  static const int vit_sms = [] {
+    const char* e = getenv("HY_VIT_SMS");
+    return e ? atoi(e) : 0;
+  }();
+  struct CapGuard {
+    bool on;
+    explicit CapGuard(int n) : on(n > 0) {
+      if (on) gemm_set_sms_cap(n);
+    }
+    ~CapGuard() {
+      if (on) gemm_set_sms_cap(0);
+    }
+  } cap_guard(vit_sms);
   // K2: patch embedding
   HY_RET_IF(hy_im2col_patches(b->images, b->n_images, b->n_patches, m->patch, m->merge, m->k_pad,
                               w.patches, st));
