@@ -804,6 +804,9 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();  // after the TMEM allocation (see gemm_tc_kernel)
+  // every CTA of the cluster must have started before a peer writes its shared memory:
+  // arrive now, wait only where it matters (before the remote stores / the final barrier)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -864,6 +867,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
     const int lrow = sub * 32 + lane;
     mbar_wait_sleepy(tfull, 0);
     tc_fence_after();
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // rank 0 has started
     const uint32_t taddr = tmem_base + ((uint32_t)(sub * 32) << 16);
     const uint32_t dst = mapa_shared(smem_u32(red + (rank - 1) * C::RED_SLOT), 0);
 #pragma unroll
@@ -880,6 +884,7 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
     }
   }
   // every thread of every CTA: the remote stores are visible to rank 0 past this barrier
+  if (!(warp >= 2 && rank != 0)) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   tc_fence_before();
   cluster_sync();
   if (rank == 0 && warp >= 2) {

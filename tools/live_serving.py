@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--requests", type=int, default=600)
     ap.add_argument("--rates", default="60,75,85")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--idle-sleep", type=float, default=1e-4, help="live loop poll sleep (s)")
+    ap.add_argument("--live-only", action="store_true")
     args = ap.parse_args()
     import torch
     import paper_2505_12658_b200 as P
@@ -42,18 +44,21 @@ def main():
                            visual_token_choices=576, prompt_dist=[25, 35, 45],
                            output_dist=[90, 110, 130], slo=slo)
         row = {"rate": rate, "requests": args.requests}
-        for mode in ("replay", "live"):
+        for mode in (("live",) if args.live_only else ("replay", "live")):
             cl = GpuCluster(spec, shape, P.b200_hardware(), slo, clock="device",
                             budgets="measured", resident_inputs=True)
             t0 = time.perf_counter()
             if mode == "live":
-                rep = run_live(cl, tr, timeout_s=1800)
+                rep = run_live(cl, tr, timeout_s=1800, idle_sleep_s=args.idle_sleep)
                 span = time.perf_counter() - t0
             else:
                 rep = cl.run(tr)
                 span = max(r.token_times[-1] for r in cl.reqs.values() if r.token_times)
             torch.cuda.synchronize()
             row[mode] = _summary(rep, span)
+            row[mode]["device_busy_s"] = sum(rt.stats["device_ms"] for rt in cl.runtimes.values()) / 1e3
+            row[mode]["host_ms_per_batch"] = (sum(rt.stats["host_ms"] for rt in cl.runtimes.values()) /
+                                              max(1, sum(rt.stats["batches"] for rt in cl.runtimes.values())))
             cl.close()
         out.append(row)
         print(json.dumps(row), flush=True)
