@@ -400,7 +400,9 @@ def run_ours(args, d: Dist):
                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
                     "traffic": traffic_of("decode_attn"), "launches_timed": s["launches"],
                     "avg_launch_ms": s["avg_ms"], "share_of_step": s["share_of_batch_time"],
-                    "peak_source": f"{peak_src} hbm_gbs"}
+                    "peak_source": f"{peak_src} hbm_gbs",
+                    # batches without vision work (no cross-stream contention)
+                    "solo_achieved": s["solo_work_per_ms"] / 1e6, "solo_launches": s["solo_launches"]}
         ach = s["work_per_ms"] / 1e9  # flop/ms -> TFLOP/s
         pk = peaks["bf16_tflops_sustained"]
         busy = s["work_per_union_ms"] / 1e9
