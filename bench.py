@@ -453,7 +453,11 @@ def run_ours(args, d: Dist):
 
     # ---- live asynchronous serving (live.py): wall-clock arrivals, concurrent instances
     live = None
-    if not args.no_live and best:
+    if emulated and not args.no_live:
+        # co-located GPU slots share one device in wall-clock time: a live run would measure
+        # that contention, not N GPUs (the replay times each batch alone instead)
+        live = {"skipped": "emulated GPU slots share one device in wall-clock time"}
+    elif not args.no_live and best:
         lp = []
         live_rate = None
         for f in (1.0, 0.9, 0.8):

@@ -304,10 +304,22 @@ def decode_sweep(out):
             cl = torch.full((n,), ctx)
         nb = -(-ctx // 16)
         be = 2 * nkv * 16 * d
-        kv = torch.randn(n * nb + 1, be, device=DEV).bfloat16()
+        # DECODE_POOL_GB: a serving-sized pool -- blocks of DECODE_LAYERS layers (block stride
+        # = layers x the one-layer slice) scattered over that many GB, as in a 122 GB KV pool
+        pool_gb = float(os.environ.get("DECODE_POOL_GB", "0"))
+        layers = int(os.environ.get("DECODE_LAYERS", "1"))
+        n_blk = n * nb + 1
+        if pool_gb > 0:
+            n_blk = max(n_blk, int(pool_gb * 1e9 // (be * layers * 2)))
+            kv = torch.empty(n_blk, be * layers, device=DEV, dtype=torch.bfloat16)
+            kv[:, :be].normal_()  # layer 0 (the one read) only
+        else:
+            kv = torch.randn(n_blk, be, device=DEV).bfloat16()
         # shuffled: blocks scattered over the pool as the free list hands them out in serving
-        ids = torch.randperm(n * nb, device=DEV) if shuffled else torch.arange(n * nb, device=DEV)
+        ids = (torch.randperm(n_blk - 1, device=DEV)[:n * nb] if shuffled
+               else torch.arange(n * nb, device=DEV))
         bt = ids.to(torch.int32).view(n, nb).contiguous()
+        be = be * layers if pool_gb > 0 else be
         q = torch.randn(n, nh * d, device=DEV).bfloat16()
         o = torch.empty_like(q)
         slots = torch.arange(n, dtype=torch.int32, device=DEV)
