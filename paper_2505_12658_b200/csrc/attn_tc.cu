@@ -427,8 +427,9 @@ __global__ void __launch_bounds__(T == 3 ? 64 + 512 : 64 + 256, 1) __maxnreg__(T
       float mx8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+      // keys 64-127 first: the registers then still hold keys 0-63 for the exp pass
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
+      for (int hh = 1; hh >= 0; --hh) {
         tmem_ld_32x32b_x32(tS + hh * 64, r);
         tmem_ld_32x32b_x32(tS + hh * 64 + 32, r + 32);
         tmem_ld_wait();
@@ -474,13 +475,14 @@ __global__ void __launch_bounds__(T == 3 ? 64 + 512 : 64 + 256, 1) __maxnreg__(T
       // columns per store; column c of P holds keys 2c, 2c+1 (already in registers)
       uint64_t rs2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
       const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2), nms2 = pk2(-ms, -ms);
-      // second read, in order: P of chunk c goes to columns [16c, 16c + 16), which belong to S
-      // chunks <= c, already read
+      // exp pass, in key order: keys 0-63 are still in registers, keys 64-127 are read again
+      // (P of chunk c goes to columns [16c, 16c + 16), which belong to S chunks <= c, already
+      // consumed; S columns 64-127 are never overwritten)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        if ((c & 1) == 0) {
-          tmem_ld_32x32b_x32(tS + c * 32, r);
-          tmem_ld_32x32b_x32(tS + c * 32 + 32, r + 32);
+        if (c == 2) {
+          tmem_ld_32x32b_x32(tS + 64, r);
+          tmem_ld_32x32b_x32(tS + 96, r + 32);
           tmem_ld_wait();
         }
         uint32_t pk[16];
