@@ -1392,14 +1392,9 @@ static const GemmTableEntry kGemmTable[] = {
 static const GemmTableEntry* gemm_table_lookup(int M, int N, int K) {
   static const bool off = getenv("HY_GEMM_NOTABLE") != nullptr;
   if (off) return nullptr;
-  const GemmTableEntry* last = nullptr;
-  for (const GemmTableEntry* e = kGemmTable; e->n; ++e) {
-    if (e->n != N || e->k != K) continue;
-    if (M <= e->m_max) return e;
-    last = e;
-  }
-  (void)last;  // beyond the measured range: the heuristic
-  return nullptr;
+  for (const GemmTableEntry* e = kGemmTable; e->n; ++e)
+    if (e->n == N && e->k == K && M <= e->m_max) return e;
+  return nullptr;  // another shape, or beyond the measured range: the heuristic
 }
 
 int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K,
