@@ -766,7 +766,9 @@ struct CskCfg {
   }
 };
 
-template <int BN, int EPI>
+// NRM = true: the normal orientation (MMA-M = 128 token rows, MMA-N = BN weight rows, tile
+// t = (token tile t % np, weight tile t / np)) for 65-256 token rows with few weight tiles
+template <int BN, int EPI, bool NRM = false>
 __global__ void __launch_bounds__(64 + 32 * 4, 1)
     gemm_swap_csk_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                          const GemmArgs a, int stages, int ks) {
@@ -786,7 +788,9 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
-  const int p = blockIdx.x / ks;  // weight tile
+  const int tile = blockIdx.x / ks;
+  const int p = NRM ? tile % a.np : tile;  // swap: weight tile; normal: token tile
+  const int q = NRM ? tile / a.np : 0;     // normal: weight tile
   const int kb0 = (int)((long long)rank * a.nkb / ks), kb1 = (int)((long long)(rank + 1) * a.nkb / ks);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmW);
@@ -813,11 +817,23 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
       // weights of the first stages before the grid dependency resolves; the activations
       // too when launched without PDL
       int npre = 0;
+      // swap: weights in the A slot (128 rows), tokens in B; normal: tokens in A, weights in B
+      auto load_w = [&](int st, int kb) {
+        if (NRM)
+          tma_load_2d(&tmW, &full[st], sB + st * C::B_BYTES, kb * C::BK, q * BN, kEvictNormal);
+        else
+          tma_load_2d(&tmW, &full[st], sA + st * C::A_BYTES, kb * C::BK, p * 128, kEvictFirst);
+      };
+      auto load_x = [&](int st, int kb) {
+        if (NRM)
+          tma_load_2d(&tmX, &full[st], sA + st * C::A_BYTES, kb * C::BK, p * 128, kEvictLast);
+        else
+          tma_load_2d(&tmX, &full[st], sB + st * C::B_BYTES, kb * C::BK, 0, kEvictLast);
+      };
       for (int kb = kb0; kb < kb1 && npre < stages; ++kb, ++npre) {
         mbar_expect_tx(&full[npre], C::STAGE_BYTES);
-        tma_load_2d(&tmW, &full[npre], sA + npre * C::A_BYTES, kb * C::BK, p * 128, kEvictFirst);
-        if (a.dbg & 16)
-          tma_load_2d(&tmX, &full[npre], sB + npre * C::B_BYTES, kb * C::BK, 0, kEvictLast);
+        load_w(npre, kb);
+        if (a.dbg & 16) load_x(npre, kb);
       }
       pdl_wait();
       int stage = 0;
@@ -825,13 +841,12 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
       int g = 0;
       for (int kb = kb0; kb < kb1; ++kb, ++g) {
         if (g < npre) {
-          if (!(a.dbg & 16))
-            tma_load_2d(&tmX, &full[stage], sB + stage * C::B_BYTES, kb * C::BK, 0, kEvictLast);
+          if (!(a.dbg & 16)) load_x(stage, kb);
         } else {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(&tmW, &full[stage], sA + stage * C::A_BYTES, kb * C::BK, p * 128, kEvictFirst);
-          tma_load_2d(&tmX, &full[stage], sB + stage * C::B_BYTES, kb * C::BK, 0, kEvictLast);
+          load_w(stage, kb);
+          load_x(stage, kb);
         }
         if (++stage == stages) {
           stage = 0;
@@ -914,8 +929,12 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
           v[j + 3] += f.w;
         }
       }
-      epi_chunk<EPI, true>(a, p * 128 + sub * 32, c * 32, v, lane,
-                           smem_u32(stg) + (warp - 2) * kStgBytes, nullptr, nst);
+      if (NRM)
+        epi_chunk<EPI, false>(a, p * 128 + sub * 32, q * BN + c * 32, v, lane,
+                              smem_u32(stg) + (warp - 2) * kStgBytes, nullptr, nst);
+      else
+        epi_chunk<EPI, true>(a, p * 128 + sub * 32, c * 32, v, lane,
+                             smem_u32(stg) + (warp - 2) * kStgBytes, nullptr, nst);
     }
   }
   tc_fence_before();
@@ -926,12 +945,12 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool NRM = false>
 static int launch_csk(const CUtensorMap& tW, const CUtensorMap& tX, const GemmArgs& a, int tiles,
                       int ks, int stages, cudaStream_t st) {
   using C = CskCfg<BN>;
   const int smem = C::smem_bytes(stages, ks);
-  auto kern = gemm_swap_csk_kernel<BN, EPI>;
+  auto kern = gemm_swap_csk_kernel<BN, EPI, NRM>;
   HY_CUDA_RET(ensure_smem(kern, 227 * 1024));
   HY_CUDA_RET(ensure_max_carveout(kern));
   HY_CUDA_RET(launch_pdl_cluster(kern, dim3(tiles * ks), dim3(C::THREADS), (size_t)smem, ks, st,
@@ -940,15 +959,15 @@ static int launch_csk(const CUtensorMap& tW, const CUtensorMap& tX, const GemmAr
   return 0;
 }
 
-template <int BN>
+template <int BN, bool NRM = false>
 static int launch_csk_epi(int epi, const CUtensorMap& tW, const CUtensorMap& tX, const GemmArgs& a,
                           int tiles, int ks, int stages, cudaStream_t st) {
   switch (epi) {
-    case EPI_BF16: return launch_csk<BN, EPI_BF16>(tW, tX, a, tiles, ks, stages, st);
-    case EPI_QGELU: return launch_csk<BN, EPI_QGELU>(tW, tX, a, tiles, ks, stages, st);
-    case EPI_GELU: return launch_csk<BN, EPI_GELU>(tW, tX, a, tiles, ks, stages, st);
-    case EPI_SWIGLU: return launch_csk<BN, EPI_SWIGLU>(tW, tX, a, tiles, ks, stages, st);
-    case EPI_F32: return launch_csk<BN, EPI_F32>(tW, tX, a, tiles, ks, stages, st);
+    case EPI_BF16: return launch_csk<BN, EPI_BF16, NRM>(tW, tX, a, tiles, ks, stages, st);
+    case EPI_QGELU: return launch_csk<BN, EPI_QGELU, NRM>(tW, tX, a, tiles, ks, stages, st);
+    case EPI_GELU: return launch_csk<BN, EPI_GELU, NRM>(tW, tX, a, tiles, ks, stages, st);
+    case EPI_SWIGLU: return launch_csk<BN, EPI_SWIGLU, NRM>(tW, tX, a, tiles, ks, stages, st);
+    case EPI_F32: return launch_csk<BN, EPI_F32, NRM>(tW, tX, a, tiles, ks, stages, st);
     default: return -1;
   }
 }
@@ -1538,6 +1557,49 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
       return (int)cudaErrorInvalidValue;
     }
     return rc;
+  }
+  // 65-256 token rows with few weight tiles (o / down projections of decode-heavy batches):
+  // normal-orientation 128 x BN tiles split over K inside a cluster (K1c, NRM), reduced
+  // through DSMEM -- the tile count that fills the most SMs wins (BN 128 or 64)
+  if (M > 64 && M <= 256 && force_mode == 0 && N % 128 == 0 && !getenv("HY_GEMM_NONCSK")) {
+    const int sms = gemm_sms();
+    const int np = ceil_div(M, 128), nkb = ceil_div(K, 64);
+    int best_bn = 0, best_ks = 0, best_st = 0, best_ctas = 0;
+    for (int cbn : {128, 64}) {
+      const int T = np * (N / cbn);
+      if (2 * T > sms) continue;
+      const int slot = 128 * cbn * 4, stage = (128 + cbn) * 64 * 2;
+      for (int ks = std::min(8, sms / T); ks >= 2; --ks) {
+        if (nkb / ks < 4) continue;
+        const int stages = std::min(8, (227 * 1024 - (ks - 1) * slot - 4 * kStgBytes - 1280) / stage);
+        if (stages < 3) continue;
+        if (T * ks > best_ctas) {
+          best_bn = cbn;
+          best_ks = ks;
+          best_st = stages;
+          best_ctas = T * ks;
+        }
+        break;
+      }
+    }
+    if (best_ks >= 2) {
+      a.np = np;
+      a.nq = N / best_bn;
+      a.nkb = nkb;
+      if (!pdl_enabled()) a.dbg |= 16;
+      CUtensorMap tW, tX;
+      HY_RET_IF(make_tmap_2d_bf16(&tX, A, M, K, (uint64_t)lda * 2, 128, 64));
+      HY_RET_IF(make_tmap_2d_bf16(&tW, W, N, K, (uint64_t)ldw * 2, best_bn, 64));
+      const int tiles = a.np * a.nq;
+      const int rc = best_bn == 128
+                         ? launch_csk_epi<128, true>(epi, tW, tX, a, tiles, best_ks, best_st, st)
+                         : launch_csk_epi<64, true>(epi, tW, tX, a, tiles, best_ks, best_st, st);
+      if (rc < 0) {
+        set_last_error("gemm: no cluster split-K kernel for this epilogue");
+        return (int)cudaErrorInvalidValue;
+      }
+      return rc;
+    }
   }
   const bool swap = (force_mode == 1) || (force_mode == 0 && M <= 256);
   int bn;

@@ -112,6 +112,19 @@ def test_gemm(M, N, K, mode, act, bias, res, f32):
     assert (out.float() - ref).abs().max().item() <= tol
 
 
+@pytest.mark.parametrize("M,N,K,act,bias,res", [
+    (100, 4096, 4096, 0, False, True),     # K1c normal orientation, BN 64, o-proj + residual
+    (256, 4096, 11008, 0, False, True),    # BN 128, down-proj + residual
+    (200, 3584, 3584, 0, True, False),     # Qwen2-VL o shape
+    (129, 1536, 512, 4, False, False),     # SwiGLU pairing, ragged token tile
+])
+def test_gemm_cluster_split_k_normal(M, N, K, act, bias, res, monkeypatch):
+    """Cluster split-K in the normal orientation (65-256 token rows), bypassing the measured
+    table so the heuristic path is exercised; checked twice for determinism."""
+    monkeypatch.setenv("HY_GEMM_NOTABLE", "1")
+    test_gemm(M, N, K, 0, act, bias, res, False)
+
+
 @pytest.mark.parametrize("M,N,K,act", [(3000, 4096, 4096, 0), (600, 2048, 4096, 1),
                                        (3328, 4096, 11008, 0)])
 def test_gemm_pair_stream_k(M, N, K, act, monkeypatch):
