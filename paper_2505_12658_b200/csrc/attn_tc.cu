@@ -325,7 +325,6 @@ __global__ void __launch_bounds__(T == 3 ? 64 + 512 : 64 + 256, 1) __maxnreg__(T
         umma_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int j) {
-        if (t == 0) mbar_wait(&v_full[j & 1], (j >> 1) & 1);
         mbar_wait(&p_full[t], j & 1);
         ATR(2 + t, j);
         tc_fence_after();
@@ -346,16 +345,26 @@ __global__ void __launch_bounds__(T == 3 ? 64 + 512 : 64 + 256, 1) __maxnreg__(T
       umma_commit(&k_empty[0]);  // K_0 retired once both Q K^T complete
       for (int j = 0; j < n_kt; ++j) {
         const bool more = j + 1 < n_kt;
-        for (int t = 0; t < C::TILES; ++t) {
-          if (t == 1 && !t1_live) continue;
-          issue_pv(t, j);
-          if (more) {
-            if (t == 0) {  // the next key tile is needed only from here on
-              mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-              ATR(1, j + 1);
-              tc_fence_after();
+        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+        // the tile whose softmax finishes first gets the tensor pipe first (the two tiles'
+        // softmaxes drift; a fixed order makes the early one wait for the late one)
+        bool done[2] = {false, !t1_live};
+        bool k_ready = false;
+        while (!(done[0] && done[1])) {
+#pragma unroll
+          for (int t = 0; t < C::TILES; ++t) {
+            if (done[t] || !mbar_test(&p_full[t], j & 1)) continue;
+            issue_pv(t, j);
+            if (more) {
+              if (!k_ready) {  // the next key tile is needed only from here on
+                mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+                ATR(1, j + 1);
+                tc_fence_after();
+                k_ready = true;
+              }
+              issue_s(t, j + 1);
             }
-            issue_s(t, j + 1);
+            done[t] = true;
           }
         }
         if (more) umma_commit(&k_empty[(j + 1) & 1]);
