@@ -479,6 +479,16 @@ inline cudaError_t ensure_max_carveout(void (*kernel)(KArgs...)) {
   return ensure_max_carveout_attr(reinterpret_cast<const void*>(kernel));
 }
 
+// Clusters of `cluster` CTAs (`threads` threads, `smem` dynamic bytes each) that can be
+// resident at once on the CURRENT device.  A cluster must fit inside one GPC, so with one
+// CTA per SM the count is not SMs / cluster (B200: GPCs of ~18 SMs hold three 5-CTA
+// clusters, not 3.7); cached per (device, kernel, cluster, smem).  0 on error.
+int max_active_clusters_attr(const void* kernel, int cluster, int threads, int smem);
+template <typename... KArgs>
+inline int max_active_clusters(void (*kernel)(KArgs...), int cluster, int threads, int smem) {
+  return max_active_clusters_attr(reinterpret_cast<const void*>(kernel), cluster, threads, smem);
+}
+
 // kernel-class timer hooks (see hy_set_kernel_timer)
 void timer_mark(int klass, cudaStream_t st, bool begin, double work, long long shape = 0);
 

@@ -918,8 +918,8 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
       float v[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-      for (int q = 0; q < ks - 1; ++q) {
-        const uint32_t src = smem_u32(red + q * C::RED_SLOT);
+      for (int r2 = 0; r2 < ks - 1; ++r2) {
+        const uint32_t src = smem_u32(red + r2 * C::RED_SLOT);
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
           const float4 f = lds_f32x4(src + (uint32_t)(((c * 8 + j / 4) * 128 + lrow) * 16));
@@ -970,6 +970,18 @@ static int launch_csk_epi(int epi, const CUtensorMap& tW, const CUtensorMap& tX,
     case EPI_F32: return launch_csk<BN, EPI_F32, NRM>(tW, tX, a, tiles, ks, stages, st);
     default: return -1;
   }
+}
+
+// Can `clusters` clusters of ks CTAs (smem bytes each) be resident at once?  A cluster sits
+// inside one GPC, so with one CTA per SM fewer ks-clusters fit than SMs / ks suggests (B200:
+// 28 clusters of 5 do not -- the Qwen2-VL down projection at M = 32 ran in two waves, 41.8 us
+// vs 26.4 us for clusters of 4).  Occupancy is the same for every epilogue instance.
+template <int BN, bool NRM>
+static bool csk_resident(int clusters, int ks, int smem) {
+  auto kern = gemm_swap_csk_kernel<BN, EPI_BF16, NRM>;
+  if (ensure_smem(kern, 227 * 1024) != cudaSuccess) return false;
+  if (ensure_max_carveout(kern) != cudaSuccess) return false;
+  return max_active_clusters(kern, ks, CskCfg<BN>::THREADS, smem) >= clusters;
 }
 
 // ---------------------------------------------------------------------------
@@ -1573,6 +1585,9 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
         if (nkb / ks < 4) continue;
         const int stages = std::min(8, (227 * 1024 - (ks - 1) * slot - 4 * kStgBytes - 1280) / stage);
         if (stages < 3) continue;
+        const int smem = stages * stage + (ks - 1) * slot + 4 * kStgBytes + 1280;
+        if (!(cbn == 128 ? csk_resident<128, true>(T, ks, smem) : csk_resident<64, true>(T, ks, smem)))
+          continue;  // the clusters would not all be resident: fewer, longer splits
         if (T * ks > best_ctas) {
           best_bn = cbn;
           best_ks = ks;
@@ -1630,15 +1645,24 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   if (swap && M <= 64 && (2 * a.np <= sms || csk_env) && !getenv("HY_GEMM_NOCSK") &&
       !(a.dbg & 2)) {
     const int cbn = M <= 32 ? 32 : 64;
+    const int stage = cbn == 32 ? CskCfg<32>::STAGE_BYTES : CskCfg<64>::STAGE_BYTES;
+    auto stages_for = [&](int k) {
+      const int red = (k - 1) * (cbn == 32 ? CskCfg<32>::RED_SLOT : CskCfg<64>::RED_SLOT);
+      const int budget = 227 * 1024 - red - 4 * kStgBytes - 1024 - 256;
+      int n = std::min(8, budget / stage);
+      if (const char* e = getenv("HY_GEMM_CSK_STAGES")) n = std::min(n, atoi(e));  // tuning
+      return n;
+    };
     int ks = std::min(8, sms / a.np);
     while (ks > 1 && a.nkb / ks < 4) --ks;
+    // every weight tile's cluster resident in one wave (clusters sit inside a GPC)
+    while (ks > 1 && stages_for(ks) >= 2 &&
+           !(cbn == 32 ? csk_resident<32, false>(a.np, ks, CskCfg<32>::smem_bytes(stages_for(ks), ks))
+                       : csk_resident<64, false>(a.np, ks, CskCfg<64>::smem_bytes(stages_for(ks), ks))))
+      --ks;
     if (csk_env) ks = std::max(1, std::min(8, atoi(csk_env)));
     if (ks >= 2) {
-      const int red = (ks - 1) * (cbn == 32 ? CskCfg<32>::RED_SLOT : CskCfg<64>::RED_SLOT);
-      const int stage = cbn == 32 ? CskCfg<32>::STAGE_BYTES : CskCfg<64>::STAGE_BYTES;
-      const int budget = 227 * 1024 - red - 4 * kStgBytes - 1024 - 256;
-      int stages = std::min(8, budget / stage);
-      if (const char* e = getenv("HY_GEMM_CSK_STAGES")) stages = std::min(stages, atoi(e));  // tuning
+      const int stages = stages_for(ks);
       if (stages >= 2) {
         a.nq = 1;
         if (!pdl_enabled()) a.dbg |= 16;

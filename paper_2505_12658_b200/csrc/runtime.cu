@@ -5,6 +5,7 @@
 #include <atomic>
 #include <map>
 #include <mutex>
+#include <tuple>
 
 namespace hy {
 
@@ -62,6 +63,34 @@ cudaError_t ensure_smem_attr(const void* kernel, int bytes) {
   e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) have = bytes;
   return e;
+}
+
+int max_active_clusters_attr(const void* kernel, int cluster, int threads, int smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int, int>, int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({dev, kernel, cluster, smem});
+  if (it != done.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();  // not sticky: clear it so the caller's next launch check is clean
+    n = 0;
+  }
+  done[{dev, kernel, cluster, smem}] = n;
+  return n;
 }
 
 cudaError_t ensure_max_carveout_attr(const void* kernel) {
