@@ -82,7 +82,8 @@ struct GemmArgs {
   int np, nq, nkb;
   int t_dp;       // whole tiles [0, t_dp) round-robin (multiple of the grid when stream-K)
   int dbg;        // bits: 1 no early PDL trigger, 2 no PDL launch (pair, HY_PAIR_DBG); 4 no residual
-                  // prefetch; 8 late PDL trigger (after the producer's last load, HY_PDL_LATE)
+                  // prefetch; 8 late PDL trigger (after the producer's last load, HY_PDL_LATE);
+                  // 16 launched without PDL; 32 K1c reduction slots inside rank 0's operand ring
   int group;      // raster group of token tiles (0 = auto; HY_GEMM_GROUP tuning only)
   long long u_sk; // k-block units of tiles [t_dp, T), split evenly over the grid
   int M, N;       // logical GEMM shape (tokens, physical weight rows)
@@ -761,8 +762,12 @@ struct CskCfg {
   static constexpr int EPI_WARPS = 4;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
-  static int smem_bytes(int stages, int ks) {
-    return stages * STAGE_BYTES + (ks - 1) * RED_SLOT + EPI_WARPS * kStgBytes + 1024 + 256;
+  // ring: the peers' partials land in rank 0's operand ring once its main loop is done, so
+  // the slots need no shared memory of their own -- the ring must hold ks - 1 of them
+  static int smem_bytes(int stages, int ks, bool ring = false) {
+    const int ops = ring ? std::max(stages * STAGE_BYTES, (ks - 1) * RED_SLOT)
+                         : stages * STAGE_BYTES + (ks - 1) * RED_SLOT;
+    return ops + EPI_WARPS * kStgBytes + 1024 + 256;
   }
 };
 
@@ -778,8 +783,11 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + stages * C::A_BYTES;
-  uint8_t* red = sB + stages * C::B_BYTES;  // [ks - 1][BN / 32][8][128] float4 (rank 0 only)
-  uint8_t* stg = red + (ks - 1) * C::RED_SLOT;
+  // [ks - 1][BN / 32][8][128] float4 (rank 0 only): behind the ring, or over it (dbg & 32)
+  const bool ring = (a.dbg & 32) != 0;
+  uint8_t* red = ring ? smem : sB + stages * C::B_BYTES;
+  uint8_t* stg = ring ? smem + std::max(stages * C::STAGE_BYTES, (ks - 1) * C::RED_SLOT)
+                      : red + (ks - 1) * C::RED_SLOT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(stg + C::EPI_WARPS * kStgBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + stages;
@@ -809,8 +817,10 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();  // after the TMEM allocation (see gemm_tc_kernel)
   // every CTA of the cluster must have started before a peer writes its shared memory:
-  // arrive now, wait only where it matters (before the remote stores / the final barrier)
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  // arrive now, wait only where it matters (before the remote stores / the final barrier).
+  // Ring mode: rank 0 arrives only once its operand ring is free (after its role below), so
+  // this barrier phase also tells the peers that the reduction slots may be written.
+  if (!(ring && rank == 0)) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -898,6 +908,16 @@ __global__ void __launch_bounds__(64 + 32 * 4, 1)
                      : "memory");
     }
   }
+  if (ring && rank == 0) {
+    // ring mode: rank 0's main loop is over once the accumulator is complete (every TMA write
+    // into the ring was consumed by an MMA that has finished reading it)
+    if (warp >= 2) {
+      mbar_wait_sleepy(tfull, 0);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  }
   // every thread of every CTA: the remote stores are visible to rank 0 past this barrier
   if (!(warp >= 2 && rank != 0)) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   tc_fence_before();
@@ -949,7 +969,7 @@ template <int BN, int EPI, bool NRM = false>
 static int launch_csk(const CUtensorMap& tW, const CUtensorMap& tX, const GemmArgs& a, int tiles,
                       int ks, int stages, cudaStream_t st) {
   using C = CskCfg<BN>;
-  const int smem = C::smem_bytes(stages, ks);
+  const int smem = C::smem_bytes(stages, ks, (a.dbg & 32) != 0);
   auto kern = gemm_swap_csk_kernel<BN, EPI, NRM>;
   HY_CUDA_RET(ensure_smem(kern, 227 * 1024));
   HY_CUDA_RET(ensure_max_carveout(kern));
@@ -970,6 +990,17 @@ static int launch_csk_epi(int epi, const CUtensorMap& tW, const CUtensorMap& tX,
     case EPI_F32: return launch_csk<BN, EPI_F32, NRM>(tW, tX, a, tiles, ks, stages, st);
     default: return -1;
   }
+}
+
+// Decode GEMMs of 65-128 token rows with a long reduction (the down projections, K >= 8192)
+// in the swap orientation with 128-wide token tiles (partials in rank 0's operand ring):
+// measured faster there (LLaVA down M = 96 28.3 -> 26.0 us, Qwen2-VL down M = 128 39.6 ->
+// 33.3) and slower for K = 3584-4096 (o M = 128 15.4 -> 17.7), which keep the normal-
+// orientation cluster split-K.  HY_GEMM_SWAP128=0 / 1 forces it off / on (A/B).
+static bool swap128_csk(int K) {
+  const char* e = getenv("HY_GEMM_SWAP128");
+  if (e) return e[0] != '0';
+  return K >= 8192;
 }
 
 // Can `clusters` clusters of ks CTAs (smem bytes each) be resident at once?  A cluster sits
@@ -1573,7 +1604,8 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   // 65-256 token rows with few weight tiles (o / down projections of decode-heavy batches):
   // normal-orientation 128 x BN tiles split over K inside a cluster (K1c, NRM), reduced
   // through DSMEM -- the tile count that fills the most SMs wins (BN 128 or 64)
-  if (M > 64 && M <= 256 && force_mode == 0 && N % 128 == 0 && !getenv("HY_GEMM_NONCSK")) {
+  if (M > (swap128_csk(K) ? 128 : 64) && M <= 256 && force_mode == 0 && N % 128 == 0 &&
+      !getenv("HY_GEMM_NONCSK")) {
     const int sms = gemm_sms();
     const int np = ceil_div(M, 128), nkb = ceil_div(K, 64);
     int best_bn = 0, best_ks = 0, best_st = 0, best_ctas = 0;
@@ -1642,13 +1674,25 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
   // decode GEMMs with few weight tiles (M <= 64, 128-row weight tiles * 2 <= SMs): split K
   // inside a cluster, reduced through distributed shared memory (K1c) -- HY_GEMM_NOCSK=1 off
   const char* csk_env = getenv("HY_GEMM_CSK");  // tuning: cluster size (any weight-tile count)
-  if (swap && M <= 64 && (2 * a.np <= sms || csk_env) && !getenv("HY_GEMM_NOCSK") &&
-      !(a.dbg & 2)) {
-    const int cbn = M <= 32 ? 32 : 64;
-    const int stage = cbn == 32 ? CskCfg<32>::STAGE_BYTES : CskCfg<64>::STAGE_BYTES;
+  if (swap && M <= (swap128_csk(K) ? 128 : 64) && (2 * a.np <= sms || csk_env) &&
+      !getenv("HY_GEMM_NOCSK") && !(a.dbg & 2)) {
+    // 65-128 token rows: 128-wide token tiles, whose 64 KB partials fit only inside rank 0's
+    // operand ring (ring mode)
+    const int cbn = M <= 32 ? 32 : M <= 64 ? 64 : 128;
+    const bool ring = cbn == 128;
+    const int stage = cbn == 32 ? CskCfg<32>::STAGE_BYTES
+                      : cbn == 64 ? CskCfg<64>::STAGE_BYTES : CskCfg<128>::STAGE_BYTES;
+    const int slot = cbn == 32 ? CskCfg<32>::RED_SLOT
+                     : cbn == 64 ? CskCfg<64>::RED_SLOT : CskCfg<128>::RED_SLOT;
+    auto smem_for = [&](int st, int k) {
+      return (ring ? std::max(st * stage, (k - 1) * slot) : st * stage + (k - 1) * slot) +
+             4 * kStgBytes + 1024 + 256;
+    };
     auto stages_for = [&](int k) {
-      const int red = (k - 1) * (cbn == 32 ? CskCfg<32>::RED_SLOT : CskCfg<64>::RED_SLOT);
-      const int budget = 227 * 1024 - red - 4 * kStgBytes - 1024 - 256;
+      const int red = (k - 1) * slot;
+      const int all = 227 * 1024 - 4 * kStgBytes - 1024 - 256;
+      if (ring && red > all) return 0;
+      const int budget = ring ? all : all - red;
       int n = std::min(8, budget / stage);
       if (const char* e = getenv("HY_GEMM_CSK_STAGES")) n = std::min(n, atoi(e));  // tuning
       return n;
@@ -1656,21 +1700,26 @@ int gemm_bf16(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int 
     int ks = std::min(8, sms / a.np);
     while (ks > 1 && a.nkb / ks < 4) --ks;
     // every weight tile's cluster resident in one wave (clusters sit inside a GPC)
-    while (ks > 1 && stages_for(ks) >= 2 &&
-           !(cbn == 32 ? csk_resident<32, false>(a.np, ks, CskCfg<32>::smem_bytes(stages_for(ks), ks))
-                       : csk_resident<64, false>(a.np, ks, CskCfg<64>::smem_bytes(stages_for(ks), ks))))
-      --ks;
+    auto resident = [&](int k) {
+      const int sm = smem_for(stages_for(k), k);
+      return cbn == 32 ? csk_resident<32, false>(a.np, k, sm)
+             : cbn == 64 ? csk_resident<64, false>(a.np, k, sm)
+                         : csk_resident<128, false>(a.np, k, sm);
+    };
+    while (ks > 1 && (stages_for(ks) < 2 || !resident(ks))) --ks;
     if (csk_env) ks = std::max(1, std::min(8, atoi(csk_env)));
     if (ks >= 2) {
       const int stages = stages_for(ks);
       if (stages >= 2) {
         a.nq = 1;
         if (!pdl_enabled()) a.dbg |= 16;
+        if (ring) a.dbg |= 32;
         CUtensorMap tW, tX;
         HY_RET_IF(make_tmap_2d_bf16(&tW, W, N, K, (uint64_t)ldw * 2, 128, 64));
         HY_RET_IF(make_tmap_2d_bf16(&tX, A, M, K, (uint64_t)lda * 2, cbn, 64));
-        const int rc = cbn == 32 ? launch_csk_epi<32>(epi, tW, tX, a, a.np, ks, stages, st)
-                                 : launch_csk_epi<64>(epi, tW, tX, a, a.np, ks, stages, st);
+        const int rc = cbn == 32   ? launch_csk_epi<32>(epi, tW, tX, a, a.np, ks, stages, st)
+                       : cbn == 64 ? launch_csk_epi<64>(epi, tW, tX, a, a.np, ks, stages, st)
+                                   : launch_csk_epi<128>(epi, tW, tX, a, a.np, ks, stages, st);
         if (rc < 0) {
           set_last_error("gemm: no cluster split-K kernel for this epilogue");
           return (int)cudaErrorInvalidValue;

@@ -69,6 +69,8 @@ def _gemm_ref(A, W, bias, act, res):
     (64, 4096, 11008, 0, 0, False, True, False),     # K1c: down-proj + residual
     (32, 4608, 3584, 0, 0, True, False, False),      # K1c: Qwen2-VL qkv (bias), 4 ranks
     (9, 4096, 512, 0, 1, True, False, False),        # K1c: short K (2 ranks), QuickGELU
+    (96, 4096, 11008, 0, 0, False, True, False),     # K1c swap BN 128 (partials in the ring), down + residual
+    (128, 3584, 18944, 0, 0, True, False, False),    # K1c swap BN 128, Qwen2-VL down shape (bias)
     (7, 12288, 512, 0, 0, False, True, False),
     (33, 1536, 512, 0, 4, False, False, False),       # swap-AB + SwiGLU (shuffle pairing)
     (64, 2816, 512, 1, 4, False, False, False),
@@ -122,6 +124,19 @@ def test_gemm_cluster_split_k_normal(M, N, K, act, bias, res, monkeypatch):
     """Cluster split-K in the normal orientation (65-256 token rows), bypassing the measured
     table so the heuristic path is exercised; checked twice for determinism."""
     monkeypatch.setenv("HY_GEMM_NOTABLE", "1")
+    monkeypatch.setenv("HY_GEMM_SWAP128", "0")  # <= 128 rows: normal orientation, not swap
+    test_gemm(M, N, K, 0, act, bias, res, False)
+
+
+@pytest.mark.parametrize("M,N,K,act,bias,res", [
+    (100, 4096, 4096, 0, False, True),     # 4 ranks, o-proj + residual
+    (128, 3584, 3584, 0, True, False),     # Qwen2-VL o shape (bias)
+    (120, 2816, 1024, 4, False, False),    # SwiGLU pairing, 2 ranks
+])
+def test_gemm_cluster_split_k_swap128(M, N, K, act, bias, res, monkeypatch):
+    """65-128 token rows in the swap orientation with 128-wide token tiles forced on for
+    short K too: the 64 KB partials go into rank 0's operand ring after its main loop."""
+    monkeypatch.setenv("HY_GEMM_SWAP128", "1")
     test_gemm(M, N, K, 0, act, bias, res, False)
 
 

@@ -1,7 +1,7 @@
 #!/bin/bash
-# decode (swap-AB / K1c) GEMMs: the dispatch's cluster split-K choice vs forced cluster sizes,
-# Qwen2-VL and LLaVA decode shapes (M <= 256), and the GEMM kernel tests
+# decode / small-M GEMMs (K1c cluster split-K): the dispatch (65-128 rows with K >= 8192 in the
+# swap orientation, 128-wide token tiles, partials in rank 0's operand ring) vs forced off / on
 cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out/csk
 timeout 300 python -m pytest tests/test_kernels_gpu.py -q -x -k gemm > gpurun_out/csk/tests.log 2>&1; echo "rc=$?" >> gpurun_out/csk/tests.log
-timeout 900 python tools/kernel_sweep.py --what gemm --only custom --shapes 32x3584x18944,64x3584x18944,32x4608x3584,64x4608x3584,32x3584x3584,64x3584x3584,32x37888x3584,128x3584x18944,256x3584x18944,128x4608x3584,256x3584x3584,32x4096x11008,64x4096x11008,32x4096x4096,128x4096x4096,256x4096x11008,16x4096x4096 --variants 'HY_GEMM_CSK=2;HY_GEMM_CSK=3;HY_GEMM_CSK=4' > gpurun_out/csk/sweep.log 2>&1
+timeout 900 python tools/kernel_sweep.py --what gemm --only custom --shapes 80x4096x11008,96x4096x11008,128x4096x11008,80x3584x18944,128x3584x18944,128x4096x4096,128x3584x3584,32x3584x18944 --variants 'HY_GEMM_SWAP128=0;HY_GEMM_SWAP128=1' > gpurun_out/csk/sweep.log 2>&1
