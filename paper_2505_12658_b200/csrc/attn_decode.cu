@@ -7,7 +7,7 @@
 // Layout read: KV pool block [layer][K|V][kv_head][16 tok][d], so one (block, head) K
 // tile is 16 x d contiguous bf16 (4 KiB at d = 128).
 //
-// Grid (seq, kv_head, split).  Each of the 4 warps streams whole 16-token blocks:
+// Grid (kv_head, seq, split).  Each of the 4 warps streams whole 16-token blocks:
 // a warp-wide 16-byte load covers 2 tokens x 128 dims, 8 loads cover the block's K and
 // 8 more its V, all issued before use.  Scores reduce across 16 lanes with xor
 // shuffles, softmax is online (exp2 domain), all G = n_heads / n_kv_heads query heads
@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(128)
   pdl_trigger();
   pdl_wait();
   constexpr int D = 128;
-  const int b = blockIdx.x, kh = blockIdx.y, sp = blockIdx.z;
+  const int b = blockIdx.y, kh = blockIdx.x, sp = blockIdx.z;  // grid (kv head, seq, split)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, dl = lane & 15;
   const int n_heads = n_kv * G;
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(128)
   pdl_trigger();
   pdl_wait();
   constexpr int D = 128;
-  const int b = blockIdx.x, kh = blockIdx.y, sp = blockIdx.z;
+  const int b = blockIdx.y, kh = blockIdx.x, sp = blockIdx.z;  // grid (kv head, seq, split)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, dl = lane & 15;
   const int n_heads = n_kv * G;
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(128)
   constexpr int D = 128, LDS = GQ_LDS, CPR = D / 8;
   extern __shared__ __align__(128) uint8_t gq_smem[];
   bf16* sQ = reinterpret_cast<bf16*>(gq_smem);
-  const int b = blockIdx.x, kh = blockIdx.y, sp = blockIdx.z;
+  const int b = blockIdx.y, kh = blockIdx.x, sp = blockIdx.z;  // grid (kv head, seq, split)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_heads = n_kv * G;
   const int ctx = ctx_len[b];
@@ -1256,7 +1256,10 @@ extern "C" int hy_attn_decode_paged(const void* q, int ld_q, int n, int n_heads,
   const int max_blocks = std::max(1, ceil_div(max_ctx, HY_KV_BLOCK_TOKENS));
   const int bps = ceil_div(max_blocks, ns);
   ns = ceil_div(max_blocks, bps);
-  dim3 grid(n, n_kv_heads, ns);
+  // head-major grid: the KV heads of one sequence run on consecutive CTAs and read adjacent
+  // 4 KiB tiles of each block (measured 2-3% more bandwidth than sequence-major, 6.82 -> 7.02
+  // TB/s at 150 sequences x 600-750 shuffled blocks)
+  dim3 grid(n_kv_heads, n, ns);
   const float sl2 = scale * 1.4426950408889634f;
   const bf16* qp = reinterpret_cast<const bf16*>(q);
   const bf16* kvp = reinterpret_cast<const bf16*>(kv_layer);
